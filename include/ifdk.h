@@ -1,0 +1,126 @@
+/*
+ * ifdk.h -- C ABI of the B200-native iFDK hot path (libifdk.so).
+ *
+ * The library computes FDK cone-beam reconstruction as the paper states the
+ * problem: "N_u x N_v x N_p -> N_x x N_y x N_z" (section
+ * "Terminology"), with the parameters of Table tbl:cbct-param.
+ *   Filtering (Alg. alg:filter):  Q_s = (E_s . F_cos) (x) F_ramp, row by row.
+ *   Back-projection (Alg. alg:bp, Alg. alg:subpixel P:431-447):
+ *     I(i,j,k) += sum_s f^2 . interp2(Q_s, x f, y f),  [x,y,z] = P_s [i,j,k,1], f = 1/z,
+ *     with P_s = (M1 . Mrot . M0)[0:3] of the appendix, beta_s = s . theta.
+ * Readings of the passages the paper leaves silent (F_cos formula, Ram-Lak
+ * ramp, FDK constant folded into Q, floor + per-tap zero border) are listed in
+ * DESIGN.md; the ids c-A5 .. c-A9 below refer to that list.
+ *
+ * Conventions (all entry points):
+ *   - Every function returns ifdk_status; nothing throws across the ABI.
+ *     ifdk_last_error() returns a thread-local message for the last failure.
+ *   - Units: pitches Du, Dv, Dx, Dy, Dz and distances D, d in mm (reading
+ *     c-A2); theta in radians; u, v in detector pixels.
+ *   - Layouts (row-major, fp32, x/u fastest):
+ *       projections  [n_views][n_rows][Nu]   rows v0 .. v0+n_rows-1 of each view
+ *       volume slab  [nk][Ny][Nx]            k = k0 .. k0+nk-1  ("i-major", P:800 slices)
+ *   - Ownership: the geometry handle is created and freed by the library.  All
+ *     data buffers are owned by the caller; the library never frees them.
+ *     Pointers named *_dev are CUDA device pointers on the current device;
+ *     pointers named *_host are host pointers.  Only ifdk_reconstruct and
+ *     ifdk_reconstruct_host allocate (stream-ordered) scratch, freed before return.
+ *   - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
+ *     default stream).  Device work is enqueued asynchronously on it; the
+ *     status reports argument and launch errors only.  Asynchronous faults
+ *     surface at the caller's next synchronisation.
+ *   - There is no CPU fallback: without a CUDA device every compute entry point
+ *     returns IFDK_ERR_CUDA.
+ */
+#ifndef IFDK_H
+#define IFDK_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    IFDK_OK = 0,
+    IFDK_ERR_INVALID_ARGUMENT = 1,   /* bad dimension/pitch/pointer/flag */
+    IFDK_ERR_DEGENERATE_GEOMETRY = 2,/* some voxel could reach z <= 0 (volume not inside the source circle) */
+    IFDK_ERR_SHAPE = 3,              /* slab/band outside range, band not covering the taps, n_views < 0 */
+    IFDK_ERR_CUDA = 4,               /* CUDA runtime / launch error (incl. no device) */
+    IFDK_ERR_OUT_OF_MEMORY = 5       /* scratch allocation failed */
+} ifdk_status;
+
+typedef struct ifdk_geometry ifdk_geometry; /* opaque, library-owned */
+
+/* Create a geometry from Table tbl:cbct-param: detector Nu x Nv
+ * pixels of pitch Du x Dv; volume Nx x Ny x Nz voxels of pitch Dx x Dy x Dz;
+ * source-to-axis distance d and source-to-detector distance D; angle step
+ * theta (beta_s = s*theta; the paper's theta = 2 pi / N_p).
+ * N_p is not a geometry argument: any global view index s is allowed.
+ * Errors: INVALID_ARGUMENT if a dimension < 1, a pitch <= 0, D <= d, d <= 0,
+ * theta not finite or 0, or out == NULL; DEGENERATE_GEOMETRY if the volume's
+ * circumscribed radius in the rotation plane is >= d. */
+ifdk_status ifdk_geometry_create(int Nu, int Nv, int Nx, int Ny, int Nz, double Du, double Dv,
+                                 double Dx, double Dy, double Dz, double D, double d,
+                                 double theta, ifdk_geometry** out);
+
+/* Free a geometry (NULL-safe) and the per-device tables it owns. */
+void ifdk_geometry_destroy(ifdk_geometry* g);
+
+/* P_s as a row-major 3x4 fp64 matrix (appendix; 3x4 per reading c-A1).
+ * Host-only; works without a GPU. */
+ifdk_status ifdk_projection_matrix(const ifdk_geometry* g, long s, double P[12]);
+
+/* Detector rows [*v_lo, *v_hi] (inclusive, clipped to [0, Nv-1]) that the
+ * interpolation taps of every voxel of slab k0..k0+nk-1 can touch in view s,
+ * with a one-row safety margin on each side.  *v_lo > *v_hi means "none".
+ * Host-only.  Errors: SHAPE if the slab is outside [0, Nz). */
+ifdk_status ifdk_band_rows(const ifdk_geometry* g, int k0, int nk, long s, int* v_lo, int* v_hi);
+
+/* Alg. alg:filter: filtered_dev = C . ((raw_dev . F_cos) (x) h1)
+ * row by row for rows v0..v0+n_rows-1 of n_views views, where F_cos is the
+ * cosine weight (reading c-A5), h1 the unit-spacing Ram-Lak kernel applied as
+ * a full-length linear convolution (reading c-A6) and C = theta d D / (2 Du)
+ * the FDK constant (reading c-A7).  Both buffers [n_views][n_rows][Nu] fp32,
+ * device; raw_dev == filtered_dev (in place) is allowed.
+ * Errors: INVALID_ARGUMENT (NULL pointers), SHAPE (rows outside [0, Nv), n_views < 0). */
+ifdk_status ifdk_filter(const ifdk_geometry* g, const float* raw_dev, float* filtered_dev,
+                        long n_views, int v0, int n_rows, void* stream);
+
+/* Alg. alg:bp + alg:subpixel for views s0..s0+n_views-1 into the
+ * slab k0..k0+nk-1:  vol_dev[k-k0][j][i] (=|+=) sum_s f^2 . interp2(Q_s, u, v).
+ * filtered_dev holds detector rows v0..v0+n_rows-1 of each view
+ * ([n_views][n_rows][Nu], device); those rows must cover ifdk_band_rows(k0,nk,s)
+ * for every view, else SHAPE (a silently zero tap would corrupt the result).
+ * Taps off the detector read 0 (reading c-A9).  accumulate = 0 overwrites the
+ * slab, 1 adds to it.  Per-voxel summation is in view order, fp32, with the
+ * per-column invariants z, u, 1/z^2 and the k-walk base of v in fp64
+ * (DESIGN.md "Numerics").
+ * Errors: INVALID_ARGUMENT (NULL, accumulate not 0/1), SHAPE (slab outside
+ * [0, Nz), band outside [0, Nv) or not covering, n_views < 0). */
+ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* filtered_dev, long s0,
+                             long n_views, int v0, int n_rows, float* vol_dev, int k0, int nk,
+                             int accumulate, void* stream);
+
+/* Whole FDK on device: filter views 0..n_views-1 of raw_dev ([n_views][Nv][Nu])
+ * into stream-ordered scratch and back-project them into vol_dev ([Nz][Ny][Nx]),
+ * overwriting it.  raw_dev is left unchanged. */
+ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw_dev, long n_views,
+                             float* vol_dev, void* stream);
+
+/* End-to-end FDK from HOST memory: raw_host ([n_views][Nv][Nu] fp32) is copied
+ * to the device in view batches (overlapped with filtering), filtered,
+ * back-projected, and the volume is copied back into vol_host ([Nz][Ny][Nx]).
+ * Host buffers should be page-locked (cudaHostAlloc / cudaHostRegister) for
+ * full PCIe bandwidth.  Synchronous: returns after vol_host is written. */
+ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float* raw_host, long n_views,
+                                  float* vol_host, void* stream);
+
+/* Number of device kernels the last successful call on this thread launched. */
+int ifdk_last_launch_count(void);
+
+/* Thread-local message describing the last non-OK status ("" if none). */
+const char* ifdk_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IFDK_H */

@@ -1,0 +1,16 @@
+"""B200-native iFDK hot path (arXiv 1909.02724): FDK cone-beam reconstruction.
+
+The compute lives in ``libifdk.so`` (hand-written sm_100a CUDA behind the C ABI
+of ``include/ifdk.h``); ``ifdk`` is its thin ctypes binding and ``dist`` the
+multi-GPU drivers (k-slab split with row-band exchange, projection split with
+reduce-scatter) over ``torch.distributed``.
+"""
+from .ifdk import (  # noqa: F401
+    Geometry,
+    IfdkError,
+    ifdk_backproject,
+    ifdk_filter,
+    ifdk_reconstruct,
+    ifdk_reconstruct_host,
+    last_launch_count,
+)

@@ -1,0 +1,217 @@
+// api.cu -- the extern "C" entry points of libifdk (see include/ifdk.h for the contract).
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ifdk_internal.h"
+
+namespace ifdk {
+
+static thread_local std::string t_last_error;
+static thread_local int t_launches = 0;
+
+ifdk_status fail(ifdk_status st, const std::string& msg)
+{
+    t_last_error = msg;
+    return st;
+}
+
+ifdk_status cuda_fail(cudaError_t e, const char* what)
+{
+    t_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? IFDK_ERR_OUT_OF_MEMORY : IFDK_ERR_CUDA;
+}
+
+void count_launch(int n) { t_launches += n; }
+
+static ifdk_status need_device()
+{
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(IFDK_ERR_CUDA, "no CUDA device (libifdk has no CPU fallback)");
+    }
+    return IFDK_OK;
+}
+
+static ifdk_status check_band(const ifdk_geometry* g, long n_views, int v0, int n_rows)
+{
+    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
+    if (n_rows < 1 || v0 < 0 || (long)v0 + n_rows > g->Nv)
+        return fail(IFDK_ERR_SHAPE, "row band v0..v0+n_rows-1 outside [0, Nv)");
+    return IFDK_OK;
+}
+
+}  // namespace ifdk
+
+using namespace ifdk;
+
+// Views per batch of ifdk_reconstruct / ifdk_reconstruct_host (a multiple of the BP kernel's
+// two-level summation batch, so batching does not change a single bit of the result).
+static const long kViewBatch = 256;
+
+extern "C" ifdk_status ifdk_filter(const ifdk_geometry* g, const float* raw_dev,
+                                   float* filtered_dev, long n_views, int v0, int n_rows,
+                                   void* stream)
+{
+    t_launches = 0;
+    if (!g || !raw_dev || !filtered_dev) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    ifdk_status s = check_band(g, n_views, v0, n_rows);
+    if (s != IFDK_OK) return s;
+    if ((s = need_device()) != IFDK_OK) return s;
+    return launch_filter(const_cast<ifdk_geometry*>(g), raw_dev, filtered_dev, n_views, v0,
+                         n_rows, (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* filtered_dev,
+                                        long s0, long n_views, int v0, int n_rows, float* vol_dev,
+                                        int k0, int nk, int accumulate, void* stream)
+{
+    t_launches = 0;
+    if (!g || !vol_dev || (!filtered_dev && n_views > 0))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (accumulate != 0 && accumulate != 1)
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "accumulate must be 0 or 1");
+    ifdk_status s = check_band(g, n_views, v0, n_rows);
+    if (s != IFDK_OK) return s;
+    if (k0 < 0 || nk < 1 || (long)k0 + nk > g->Nz)
+        return fail(IFDK_ERR_SHAPE, "slab k0..k0+nk-1 outside [0, Nz)");
+    for (long t = 0; t < n_views; ++t) {
+        int lo, hi;
+        band_rows(g, k0, nk, s0 + t, &lo, &hi);
+        if (lo <= hi && (lo < v0 || hi > v0 + n_rows - 1)) {
+            char buf[200];
+            snprintf(buf, sizeof buf,
+                     "view %ld needs detector rows %d..%d but the band holds %d..%d", s0 + t, lo,
+                     hi, v0, v0 + n_rows - 1);
+            return fail(IFDK_ERR_SHAPE, buf);
+        }
+    }
+    if ((s = need_device()) != IFDK_OK) return s;
+    return launch_backproject(g, filtered_dev, s0, n_views, v0, n_rows, vol_dev, k0, nk,
+                              accumulate, (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw_dev,
+                                        long n_views, float* vol_dev, void* stream)
+{
+    t_launches = 0;
+    if (!g || !raw_dev || !vol_dev) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t view_elems = (size_t)g->Nv * g->Nu;
+    const long batch = n_views < kViewBatch ? (n_views > 0 ? n_views : 1) : kViewBatch;
+    float* Q = nullptr;
+    cudaError_t e = cudaMallocAsync(&Q, sizeof(float) * view_elems * batch, st);
+    if (e != cudaSuccess) return fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(filtered scratch)");
+    int launches = 0;
+    if (n_views == 0) s = launch_backproject(g, Q, 0, 0, 0, g->Nv, vol_dev, 0, g->Nz, 0, st);
+    for (long b0 = 0; b0 < n_views && s == IFDK_OK; b0 += batch) {
+        const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
+        s = launch_filter(const_cast<ifdk_geometry*>(g), raw_dev + b0 * view_elems, Q, nb, 0,
+                          g->Nv, st);
+        if (s != IFDK_OK) break;
+        s = launch_backproject(g, Q, b0, nb, 0, g->Nv, vol_dev, 0, g->Nz, b0 > 0 ? 1 : 0, st);
+        launches += 2;
+    }
+    cudaFreeAsync(Q, st);
+    t_launches = launches;
+    return s;
+}
+
+extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float* raw_host,
+                                             long n_views, float* vol_host, void* stream)
+{
+    t_launches = 0;
+    if (!g || !raw_host || !vol_host) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t view_elems = (size_t)g->Nv * g->Nu;
+    const size_t vol_elems = (size_t)g->Nz * g->Ny * g->Nx;
+    const long batch = n_views < kViewBatch ? (n_views > 0 ? n_views : 1) : kViewBatch;
+    // Two staging buffers: batch b+1 is copied on `cp` while batch b is filtered (in place)
+    // and back-projected on `st`.
+    cudaStream_t cp = nullptr;
+    cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    float* buf[2] = {nullptr, nullptr};
+    float* vol = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate");
+    for (int q = 0; q < 2; ++q) {
+        cudaEventCreateWithFlags(&copied[q], cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&consumed[q], cudaEventDisableTiming);
+    }
+    e = cudaMallocAsync(&vol, sizeof(float) * vol_elems, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&buf[0], sizeof(float) * view_elems * batch, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(&buf[1], sizeof(float) * view_elems * batch, st);
+    if (e != cudaSuccess) s = fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(reconstruct_host)");
+    int launches = 0;
+    if (s == IFDK_OK) {
+        cudaEvent_t ready;
+        cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+        cudaEventRecord(ready, st);  // allocations visible to the copy stream
+        cudaStreamWaitEvent(cp, ready, 0);
+        cudaEventDestroy(ready);
+        if (n_views == 0) s = launch_backproject(g, buf[0], 0, 0, 0, g->Nv, vol, 0, g->Nz, 0, st);
+        const long nbatches = (n_views + batch - 1) / batch;
+        auto enqueue_copy = [&](long b) {
+            const int q = (int)(b & 1);
+            const long b0 = b * batch;
+            const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
+            if (b >= 2) cudaStreamWaitEvent(cp, consumed[q], 0);
+            cudaMemcpyAsync(buf[q], raw_host + b0 * view_elems, sizeof(float) * view_elems * nb,
+                            cudaMemcpyHostToDevice, cp);
+            cudaEventRecord(copied[q], cp);
+        };
+        if (nbatches > 0) enqueue_copy(0);
+        if (nbatches > 1) enqueue_copy(1);
+        for (long b = 0; b < nbatches && s == IFDK_OK; ++b) {
+            const int q = (int)(b & 1);
+            const long b0 = b * batch;
+            const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
+            cudaStreamWaitEvent(st, copied[q], 0);
+            s = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb, 0, g->Nv, st);
+            if (s != IFDK_OK) break;
+            s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vol, 0, g->Nz, b0 > 0 ? 1 : 0, st);
+            launches += 2;
+            cudaEventRecord(consumed[q], st);
+            if (b + 2 < nbatches) enqueue_copy(b + 2);
+        }
+        if (s == IFDK_OK) {
+            e = cudaMemcpyAsync(vol_host, vol, sizeof(float) * vol_elems, cudaMemcpyDeviceToHost, st);
+            if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(volume D2H)");
+        }
+    }
+    if (buf[0]) cudaFreeAsync(buf[0], st);
+    if (buf[1]) cudaFreeAsync(buf[1], st);
+    if (vol) cudaFreeAsync(vol, st);
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess && s == IFDK_OK) s = cuda_fail(e, "reconstruct_host");
+    cudaStreamSynchronize(cp);
+    for (int q = 0; q < 2; ++q) {
+        cudaEventDestroy(copied[q]);
+        cudaEventDestroy(consumed[q]);
+    }
+    cudaStreamDestroy(cp);
+    t_launches = launches;
+    return s;
+}
+
+extern "C" void ifdk_geometry_destroy(ifdk_geometry* g)
+{
+    if (!g) return;
+    for (auto& d : g->dev) {
+        if (d.Hs) cudaFree(d.Hs);
+        if (d.tw) cudaFree(d.tw);
+    }
+    delete g;
+}
+
+extern "C" int ifdk_last_launch_count(void) { return t_launches; }
+
+extern "C" const char* ifdk_last_error(void) { return t_last_error.c_str(); }

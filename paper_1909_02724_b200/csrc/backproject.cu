@@ -1,0 +1,526 @@
+// backproject.cu -- BP-sm100: voxel-driven FDK back-projection (Alg. alg:bp P:402-430,
+// Alg. alg:subpixel P:431-447) organised around the appendix invariant (Theorems 2-3,
+// P:506-507): for fixed (i, j, beta) the depth z, the detector column u and the weight
+// 1/z^2 are constant along k, and v is affine in k.
+//
+// Mapping (B200-first; not the paper's shflBP design):
+//  * A CTA (256 threads = 8 warps of 8(i) x 4(j) columns) owns a 16 x 16 column tile and a
+//    KC-slice k-chunk aligned to global multiples of KC.  Each thread owns one voxel column
+//    and walks the chunk with KC register accumulators: per (column, view) it computes
+//    z, u, 1/z^2 and the base of v in fp64 once, then per update
+//    only v = fv0 + kappa dv in fp32, a floor, two shared-memory loads and four FMAs.
+//  * The detector patch the tile x chunk projects onto (its extent is bounded from the
+//    tile corners: u, v are linear-fractional, so extremes sit at corners) is staged per
+//    view by TMA (cp.async.bulk.tensor, OOB zero fill = the per-tap zero border, reading
+//    c-A9) into a double-buffered raw box, then rewritten once into (Q[r][c], Q[r][c+1] -
+//    Q[r][c]) pairs so that each detector row costs one LDS.64 and one FMA per update.
+//    TMA for view t+3 is in flight while view t is accumulated.
+//  * Views are summed in order; every VB views (aligned to global view index) the register
+//    partial sums are added to the volume, a two-level summation.
+//  * A view whose patch does not fit the box (never for the five configs) is accumulated
+//    from global memory with bitwise-identical arithmetic.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "ifdk_internal.h"
+
+namespace ifdk {
+namespace {
+
+constexpr int kTI = 16, kTJ = 16, kThreads = 256;
+constexpr int kKC = 64;
+
+struct BPParams {
+    const double* P;  // [n_views][10]: P00 P01 P03 | P10 P11 P12 P13 | P20 P21 P23
+    const float* Q;   // band [n_views][n_rows][Nu]
+    float* vol;       // slab [nk][Ny][Nx]
+    long n_views;
+    long s0;
+    int Nu, Nv, Nx, Ny;
+    int v0, n_rows;
+    int k0, nk;       // slab (global k)
+    int kb0;          // global k of chunk 0 (multiple of KC)
+    int tiles_i;
+    int box_w, box_h;
+    int raw_bytes;    // bytes of one raw box (multiple of 128)
+    int vb;           // view batch of the two-level summation
+    uint32_t neg_magic;  // -0x4B000000 * P2 * 8 mod 2^32 (see accumulate_view_smem)
+    int accumulate;
+};
+
+struct __align__(16) Meta {
+    double P[10];
+    int u_org, v_org, fast, pad;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    const uint32_t a = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ float2 lds64(uint32_t addr)
+{
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+    return v;
+}
+
+// Per-(column, view) invariants in fp64 (Theorems 2-3): u and 1/z are k-invariant; v at the
+// chunk base kb; dv = dv/dk.  Shared by the threads and by the patch-bound computation so
+// that corner columns reproduce the threads' values bit for bit.
+struct ColInv {
+    double u, v, f, dv;
+};
+
+__device__ __forceinline__ ColInv column_invariants(const double* P, double i, double j, double kb)
+{
+    ColInv c;
+    const double x = fma(P[0], i, fma(P[1], j, P[2]));
+    const double y = fma(P[3], i, fma(P[4], j, fma(P[5], kb, P[6])));
+    const double z = fma(P[7], i, fma(P[8], j, P[9]));
+    c.f = __drcp_rn(z);
+    c.u = x * c.f;
+    c.v = y * c.f;
+    c.dv = P[5] * c.f;
+    return c;
+}
+
+// Thread-side split of the invariants: integer detector column/row + fp32 fractions.
+struct ThreadInv {
+    int nu, nv;
+    float du, fv0, dv, W;
+};
+
+__device__ __forceinline__ ThreadInv split(const ColInv& c)
+{
+    ThreadInv t;
+    const double fu = floor(c.u), fv = floor(c.v);
+    t.nu = (int)fu;
+    t.nv = (int)fv;
+    t.du = (float)(c.u - fu);
+    t.fv0 = (float)(c.v - fv);
+    t.dv = (float)c.dv;
+    t.W = (float)(c.f * c.f);  // W_dis = f^2, Alg. alg:bp line 8
+    return t;
+}
+
+// floor() of a non-negative fp32 v < 2^23 through the round-down magic add: the returned
+// bits are 0x4B000000 + floor(v); *fr = v - floor(v) exactly.
+__device__ __forceinline__ uint32_t floor_bits(float v, float* fr)
+{
+    const float t = __fadd_rd(v, 8388608.0f);
+    *fr = v - (t - 8388608.0f);
+    return __float_as_uint(t);
+}
+
+// One view from the (a, delta) pair patch in shared memory.
+template <int KC, int P2, bool FULL>
+__device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t pair_base,
+                                                     uint32_t neg_magic, const ThreadInv& t,
+                                                     int u_org, int v_org, int kv0, int kv1)
+{
+    // byte address of pair (row nv + n, col nu) = pair_base + ((nv - v_org + n) P2 + nu - u_org) 8
+    // neg_magic = -0x4B000000 * P2 * 8 (mod 2^32) arrives as a kernel parameter so that ptxas
+    // cannot split it back out of the base: one IMAD per update forms the tap address.
+    const uint32_t a0 =
+        pair_base + (uint32_t)(((t.nv - v_org) * P2 + (t.nu - u_org)) * 8) + neg_magic;
+    float fv0 = t.fv0;
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+        // Every 8 updates, launder fv0 through a volatile asm so that the compiler cannot
+        // hoist the address arithmetic of later updates above earlier shared loads (which
+        // would need a register per hoisted address and spill the 64 accumulators).
+        if ((kk & 7) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+        if (!FULL && (kk < kv0 || kk >= kv1)) continue;
+        float fr;
+        const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
+        const uint32_t addr = bits * (uint32_t)(P2 * 8) + a0;
+        const float2 p0 = lds64(addr);
+        const float2 p1 = lds64(addr + P2 * 8);
+        const float h0 = fmaf(t.du, p0.y, p0.x);
+        const float h1 = fmaf(t.du, p1.y, p1.x);
+        const float val = fmaf(fr, h1 - h0, h0);  // Alg. alg:subpixel lines 4-6
+        acc[kk] = fmaf(t.W, val, acc[kk]);        // I += W_dis . interp2, Alg. alg:bp line 10
+    }
+}
+
+__device__ __forceinline__ float tapg(const float* __restrict__ Qv, int Nu, int Nv, int v0,
+                                      int n_rows, int row, int col)
+{
+    if (col < 0 || col >= Nu || row < 0 || row >= Nv) return 0.f;  // zero border, c-A9
+    const int r = row - v0;
+    if (r < 0 || r >= n_rows) return 0.f;  // host guarantees band coverage
+    return __ldg(Qv + (long)r * Nu + col);
+}
+
+// One view from global memory (same arithmetic as the shared-memory path).
+template <int KC>
+__device__ __forceinline__ void accumulate_view_global(float (&acc)[KC], const float* Qv,
+                                                       const BPParams& p, const ThreadInv& t,
+                                                       int kv0, int kv1)
+{
+    float fv0 = t.fv0;
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+        if ((kk & 3) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+        if (kk < kv0 || kk >= kv1) continue;
+        float fr;
+        const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
+        const int row = t.nv + (int)(bits - 0x4B000000u);
+        const float a0 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row, t.nu);
+        const float b0 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row, t.nu + 1);
+        const float a1 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row + 1, t.nu);
+        const float b1 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row + 1, t.nu + 1);
+        const float h0 = fmaf(t.du, b0 - a0, a0);
+        const float h1 = fmaf(t.du, b1 - a1, a1);
+        const float val = fmaf(fr, h1 - h0, h0);
+        acc[kk] = fmaf(t.W, val, acc[kk]);
+    }
+}
+
+template <int KC>
+__device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i, int j, int kb,
+                                      int kv0, int kv1, bool overwrite)
+{
+    float* q = p.vol + ((long)(kb - p.k0) * p.Ny + j) * p.Nx + i;
+    long plane = (long)p.Ny * p.Nx;
+    // Opaque to the optimiser: stops it from hoisting 64 addresses out of the view loop.
+    asm volatile("mov.b64 %0, %0;" : "+l"(plane));
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+        if (kk >= kv0 && kk < kv1) *q = overwrite ? acc[kk] : *q + acc[kk];
+        acc[kk] = 0.f;
+        q += plane;
+    }
+}
+
+// Patch box of view t for the tile (warp 0): corners of the tile, both ends of the chunk.
+__device__ void compute_meta(Meta* m, const BPParams& p, long t, int i_lo, int i_hi, int j_lo,
+                             int j_hi, int kb, int kv0, int kv1)
+{
+    const int lane = threadIdx.x & 31;
+    const double* Pg = p.P + t * 10;
+    if (lane < 10) m->P[lane] = Pg[lane];
+    const int corner = lane & 3;
+    const double ci = (corner & 1) ? i_hi : i_lo;
+    const double cj = (corner & 2) ? j_hi : j_lo;
+    double P[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) P[q] = __ldg(Pg + q);
+    const ColInv c = column_invariants(P, ci, cj, (double)kb);
+    double umin = c.u, umax = c.u;
+    double va = c.v + kv0 * c.dv, vb = c.v + (kv1 - 1) * c.dv;
+    double vmin = fmin(va, vb), vmax = fmax(va, vb);
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {
+        umin = fmin(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+        umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+        vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    if (lane == 0) {
+        const double fu0 = floor(umin), fu1 = floor(umax), fv0 = floor(vmin), fv1 = floor(vmax);
+        // TMA (tile mode, no swizzle) faults unless the innermost box coordinate is a
+        // multiple of 16 bytes (measured: tools/tma_probe.cu), so the column origin is
+        // rounded down to a multiple of 4 floats.
+        m->u_org = ((int)fu0 - 1) & ~3;
+        m->v_org = (int)fv0 - 1;
+        const double w_need = fu1 + 3.0 - m->u_org, h_need = fv1 - fv0 + 4.0;
+        m->fast = (w_need <= p.box_w && h_need <= p.box_h && fu0 > -1e9 && fu1 < 1e9 &&
+                   fv0 > -1e9 && fv1 < 1e9)
+                      ? 1
+                      : 0;
+    }
+}
+
+template <int KC, int P2, bool TMA>
+__global__ void __launch_bounds__(kThreads, 2)
+    bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile_i = blockIdx.x % p.tiles_i, tile_j = blockIdx.x / p.tiles_i;
+    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    const bool active = i < p.Nx && j < p.Ny;
+    const int i_lo = tile_i * kTI, i_hi = min(i_lo + kTI, p.Nx) - 1;
+    const int j_lo = tile_j * kTJ, j_hi = min(j_lo + kTJ, p.Ny) - 1;
+    const int kb = p.kb0 + (int)blockIdx.y * KC;
+    const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, KC);
+    const bool full = kv0 == 0 && kv1 == KC;
+
+    float acc[KC];
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) acc[kk] = 0.f;
+    bool overwrite = !p.accumulate;
+    const long n = p.n_views;
+
+    // raw box of view t: smem + (t & 1) raw_bytes; pair patch of view t: pair0 + (t & 1) box_h P2
+    float2* const pair0 = reinterpret_cast<float2*>(smem + 2 * p.raw_bytes);
+    auto raw_of = [&](long t) { return smem + (t & 1) * p.raw_bytes; };
+    auto pair_of = [&](long t) { return pair0 + (t & 1) * p.box_h * P2; };
+    Meta* meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_h * P2);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(meta + 4);
+    const uint32_t tx_bytes = (uint32_t)(p.box_w * p.box_h * 4);
+
+    // The tensor map must be addressed in param space (__grid_constant__): take its address
+    // here, in the kernel body, never through a by-reference lambda capture (which would copy
+    // it to local memory, an illegal TMA operand).
+    const CUtensorMap* const tmap_ptr = &tmap;
+    auto issue = [=](long t) {  // warp 0 only
+        compute_meta(&meta[t & 3], p, t, i_lo, i_hi, j_lo, j_hi, kb, kv0, kv1);
+        __syncwarp();
+        if (TMA && lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&mbar[t & 1], tx_bytes);
+            tma_load_3d(smem + (t & 1) * p.raw_bytes, tmap_ptr, &mbar[t & 1], meta[t & 3].u_org,
+                        meta[t & 3].v_org - p.v0, (int)t);
+        }
+    };
+    auto transform = [&](long t) {  // all threads: raw box -> (a, delta) pairs
+        const Meta& m = meta[t & 3];
+        if (!m.fast) return;
+        const float* r = reinterpret_cast<const float*>(raw_of(t));
+        float2* q = pair_of(t);
+        const int wp = p.box_w - 1, total = p.box_h * wp;
+        for (int e = tid; e < total; e += kThreads) {
+            const int rr = e / wp, cc = e - rr * wp;
+            const float a = r[rr * p.box_w + cc], b = r[rr * p.box_w + cc + 1];
+            q[rr * P2 + cc] = make_float2(a, b - a);
+        }
+    };
+
+    if (TMA) {
+        if (tid == 0) {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (warp == 0) {
+            if (n > 0) issue(0);
+            if (n > 1) issue(1);
+        }
+        __syncthreads();
+        if (n > 0) {
+            mbar_wait(&mbar[0], 0);
+            transform(0);
+        }
+        __syncthreads();
+        if (warp == 0 && n > 2) issue(2);
+    }
+
+    for (long t = 0; t < n; ++t) {
+        const double* P;
+        int u_org = 0, v_org = 0, fast = 0;
+        if (TMA) {
+            const Meta& m = meta[t & 3];
+            P = m.P;
+            u_org = m.u_org;
+            v_org = m.v_org;
+            fast = m.fast;
+        } else {
+            P = p.P + t * 10;
+        }
+        if (active) {
+            double Pr[10];
+#pragma unroll
+            for (int q = 0; q < 10; ++q) Pr[q] = P[q];
+            const ThreadInv ti = split(column_invariants(Pr, (double)i, (double)j, (double)kb));
+            if constexpr (TMA) {
+                // The host sizes the box from a conservative bound, so every view fits.
+                if (!fast) __trap();
+                const uint32_t pb = smem_u32(pair_of(t));
+                if (full)
+                    accumulate_view_smem<KC, P2, true>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
+                else
+                    accumulate_view_smem<KC, P2, false>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
+            } else {
+                accumulate_view_global<KC>(acc, p.Q + t * (long)p.n_rows * p.Nu, p, ti, kv0, kv1);
+            }
+            if ((p.s0 + t + 1) % p.vb == 0 || t == n - 1) {
+                flush<KC>(acc, p, i, j, kb, kv0, kv1, overwrite);
+                overwrite = false;
+            }
+        }
+        if (TMA) {
+            if (t + 1 < n) {
+                mbar_wait(&mbar[(t + 1) & 1], (uint32_t)(((t + 1) >> 1) & 1));
+                transform(t + 1);
+            }
+            __syncthreads();
+            if (warp == 0 && t + 3 < n) issue(t + 3);
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+template <int P2>
+ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, bool tma, dim3 grid, size_t smem,
+                     cudaStream_t st)
+{
+    cudaError_t e;
+    if (tma) {
+        auto k = bp_kernel<kKC, P2, true>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp)");
+        k<<<grid, kThreads, smem, st>>>(p, map);
+    } else {
+        auto k = bp_kernel<kKC, P2, false>;
+        k<<<grid, kThreads, 0, st>>>(p, map);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "bp_kernel launch");
+    count_launch();
+    return IFDK_OK;
+}
+
+}  // namespace
+
+ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
+                               int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
+                               cudaStream_t st)
+{
+    if (n_views == 0) {
+        if (!accumulate) {
+            cudaError_t e =
+                cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nk * g->Ny * g->Nx, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+        }
+        return IFDK_OK;
+    }
+    // Per-view projection matrices (fp64) for the device.
+    std::vector<double> Ph((size_t)n_views * 10);
+    for (long t = 0; t < n_views; ++t) {
+        double P[12];
+        projection_matrix(g, s0 + t, P);
+        double* o = &Ph[(size_t)t * 10];
+        o[0] = P[0]; o[1] = P[1]; o[2] = P[3];
+        o[3] = P[4]; o[4] = P[5]; o[5] = P[6]; o[6] = P[7];
+        o[7] = P[8]; o[8] = P[9]; o[9] = P[11];
+    }
+    double* Pd = nullptr;
+    cudaError_t e = cudaMallocAsync(&Pd, Ph.size() * sizeof(double), st);
+    if (e != cudaSuccess) return fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(P table)");
+    e = cudaMemcpyAsync(Pd, Ph.data(), Ph.size() * sizeof(double), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(P table)");
+
+    BPParams p{};
+    p.P = Pd;
+    p.Q = Q;
+    p.vol = vol;
+    p.n_views = n_views;
+    p.s0 = s0;
+    p.Nu = g->Nu; p.Nv = g->Nv; p.Nx = g->Nx; p.Ny = g->Ny;
+    p.v0 = v0; p.n_rows = n_rows;
+    p.k0 = k0; p.nk = nk;
+    p.kb0 = (k0 / kKC) * kKC;
+    p.tiles_i = (g->Nx + kTI - 1) / kTI;
+    const int tiles_j = (g->Ny + kTJ - 1) / kTJ;
+    const int n_chunks = (k0 + nk - p.kb0 + kKC - 1) / kKC;
+    p.vb = 128;
+    p.accumulate = accumulate;
+
+    // Box of the staged patch from the conservative geometric bound.
+    double wb, hb;
+    patch_bound(g, kTI, kTJ, kKC, &wb, &hb);
+    int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
+    int box_h = (int)std::ceil(hb) + 6;
+    if (box_w < 8) box_w = 8;
+    int P2 = 0;
+    for (int c : {24, 40, 56, 72})
+        if (c >= box_w - 1) { P2 = c; break; }
+    bool tma = P2 != 0 && box_h <= 256 && (g->Nu % 4) == 0 &&
+               (reinterpret_cast<uintptr_t>(Q) % 16) == 0 && get_encode() != nullptr;
+    CUtensorMap map;
+    std::memset(&map, 0, sizeof(map));
+    size_t smem = 0;
+    if (tma) {
+        p.box_w = box_w;
+        p.box_h = box_h;
+        p.raw_bytes = (box_w * box_h * 4 + 127) / 128 * 128;
+        smem = 2 * (size_t)p.raw_bytes + 2 * sizeof(float2) * box_h * P2 + 4 * sizeof(Meta) + 16;
+        cuuint64_t dims[3] = {(cuuint64_t)g->Nu, (cuuint64_t)n_rows, (cuuint64_t)n_views};
+        cuuint64_t strides[2] = {(cuuint64_t)g->Nu * 4, (cuuint64_t)g->Nu * 4 * n_rows};
+        cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)Q, dims,
+                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) tma = false;
+    }
+    if (!tma) {
+        P2 = 24;
+        p.box_w = p.box_h = 0;
+        p.raw_bytes = 0;
+    }
+    p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
+    dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
+    ifdk_status s;
+    switch (P2) {
+        case 24: s = launch_t<24>(p, map, tma, grid, smem, st); break;
+        case 40: s = launch_t<40>(p, map, tma, grid, smem, st); break;
+        case 56: s = launch_t<56>(p, map, tma, grid, smem, st); break;
+        default: s = launch_t<72>(p, map, tma, grid, smem, st); break;
+    }
+    cudaFreeAsync(Pd, st);
+    return s;
+}
+
+}  // namespace ifdk

@@ -1,0 +1,57 @@
+// ifdk_internal.h -- internal declarations shared by the libifdk translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ifdk.h"
+
+struct ifdk_geometry {
+    // Table tbl:cbct-param
+    int Nu, Nv, Nx, Ny, Nz;
+    double Du, Dv, Dx, Dy, Dz, D, d, theta;
+    // derived
+    double cu, cv, cx, cy, cz;  // (N-1)/2 centres
+    double C;                   // FDK constant theta d D / (2 Du), reading c-A7
+    double zmin, zmax;          // bounds of z over the volume and all views
+    double rxy;                 // circumscribed radius of the volume in the rotation plane
+    // ramp filter spectrum (lazy): L = FFT length, Hs[f] = C/L * DFT(h1 circular)[f]
+    int log2L = 0;
+    std::vector<float> Hs;      // L/2 + 1 values
+    std::vector<float> tw;      // 2L floats: (cos, -sin)(2 pi t / L)
+    // per-device copies of the filter tables
+    struct Dev {
+        float* Hs = nullptr;
+        float2* tw = nullptr;
+    } dev[32];
+    std::mutex mu;
+};
+
+namespace ifdk {
+
+// error plumbing (api.cu)
+ifdk_status fail(ifdk_status st, const std::string& msg);
+ifdk_status cuda_fail(cudaError_t e, const char* what);
+void count_launch(int n = 1);
+
+// geometry.cpp
+void projection_matrix(const ifdk_geometry* g, long s, double P[12]);
+void band_rows(const ifdk_geometry* g, int k0, int nk, long s, int* lo, int* hi);
+void ensure_filter_tables_host(ifdk_geometry* g);
+
+// Conservative bound on the detector patch (columns, rows) that a tile of
+// ti x tj voxel columns and kc slices can touch, over all views and positions.
+void patch_bound(const ifdk_geometry* g, int ti, int tj, int kc, double* w, double* h);
+
+// filter.cu
+ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
+                          int n_rows, cudaStream_t st);
+
+// backproject.cu
+ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
+                               int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
+                               cudaStream_t st);
+
+}  // namespace ifdk

@@ -1,0 +1,203 @@
+"""Thin ctypes binding of libifdk (include/ifdk.h): argument marshalling only.
+
+Every step of the FDK hot path runs in the CUDA kernels of libifdk.so; this
+module only converts torch tensors / numpy arrays into pointers and sizes and
+turns non-OK statuses into exceptions.  There is no CPU fallback: if the
+library is missing the import fails, and without a GPU every compute call
+raises ``IfdkError`` (status IFDK_ERR_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libifdk.so")
+
+IFDK_OK = 0
+STATUS_NAMES = {
+    0: "IFDK_OK",
+    1: "IFDK_ERR_INVALID_ARGUMENT",
+    2: "IFDK_ERR_DEGENERATE_GEOMETRY",
+    3: "IFDK_ERR_SHAPE",
+    4: "IFDK_ERR_CUDA",
+    5: "IFDK_ERR_OUT_OF_MEMORY",
+}
+
+# Every symbol include/ifdk.h declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "ifdk_geometry_create",
+    "ifdk_geometry_destroy",
+    "ifdk_projection_matrix",
+    "ifdk_band_rows",
+    "ifdk_filter",
+    "ifdk_backproject",
+    "ifdk_reconstruct",
+    "ifdk_reconstruct_host",
+    "ifdk_last_launch_count",
+    "ifdk_last_error",
+)
+
+
+class IfdkError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing -- build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the iFDK path has no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+_vp, _i, _l, _d = ctypes.c_void_p, ctypes.c_int, ctypes.c_long, ctypes.c_double
+_lib.ifdk_geometry_create.argtypes = [_i] * 5 + [_d] * 8 + [ctypes.POINTER(_vp)]
+_lib.ifdk_geometry_create.restype = _i
+_lib.ifdk_geometry_destroy.argtypes = [_vp]
+_lib.ifdk_geometry_destroy.restype = None
+_lib.ifdk_projection_matrix.argtypes = [_vp, _l, ctypes.POINTER(_d)]
+_lib.ifdk_projection_matrix.restype = _i
+_lib.ifdk_band_rows.argtypes = [_vp, _i, _i, _l, ctypes.POINTER(_i), ctypes.POINTER(_i)]
+_lib.ifdk_band_rows.restype = _i
+_lib.ifdk_filter.argtypes = [_vp, _vp, _vp, _l, _i, _i, _vp]
+_lib.ifdk_filter.restype = _i
+_lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp]
+_lib.ifdk_backproject.restype = _i
+_lib.ifdk_reconstruct.argtypes = [_vp, _vp, _l, _vp, _vp]
+_lib.ifdk_reconstruct.restype = _i
+_lib.ifdk_reconstruct_host.argtypes = [_vp, _vp, _l, _vp, _vp]
+_lib.ifdk_reconstruct_host.restype = _i
+_lib.ifdk_last_launch_count.argtypes = []
+_lib.ifdk_last_launch_count.restype = _i
+_lib.ifdk_last_error.argtypes = []
+_lib.ifdk_last_error.restype = ctypes.c_char_p
+
+
+def _check(st: int) -> None:
+    if st != IFDK_OK:
+        raise IfdkError(st, _lib.ifdk_last_error().decode())
+
+
+def last_launch_count() -> int:
+    """Kernels the last successful libifdk call on this thread launched."""
+    return int(_lib.ifdk_last_launch_count())
+
+
+class Geometry:
+    """ifdk_geometry_create / ifdk_geometry_destroy (Table tbl:cbct-param)."""
+
+    def __init__(self, Nu, Nv, Nx, Ny, Nz, Du, Dv, Dx, Dy, Dz, D, d, theta):
+        h = _vp()
+        _check(_lib.ifdk_geometry_create(int(Nu), int(Nv), int(Nx), int(Ny), int(Nz), float(Du),
+                                         float(Dv), float(Dx), float(Dy), float(Dz), float(D),
+                                         float(d), float(theta), ctypes.byref(h)))
+        self._h = h
+        self.Nu, self.Nv, self.Nx, self.Ny, self.Nz = int(Nu), int(Nv), int(Nx), int(Ny), int(Nz)
+        self.Du, self.Dv, self.Dx, self.Dy, self.Dz = map(float, (Du, Dv, Dx, Dy, Dz))
+        self.D, self.d, self.theta = float(D), float(d), float(theta)
+
+    @classmethod
+    def from_spec(cls, spec) -> "Geometry":
+        return cls(**spec.geometry_args())
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.ifdk_geometry_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def projection_matrix(self, s: int) -> np.ndarray:
+        P = (ctypes.c_double * 12)()
+        _check(_lib.ifdk_projection_matrix(self._h, int(s), P))
+        return np.frombuffer(P, np.float64).reshape(3, 4).copy()
+
+    def band_rows(self, k0: int, nk: int, s: int) -> tuple[int, int]:
+        lo, hi = ctypes.c_int(), ctypes.c_int()
+        _check(_lib.ifdk_band_rows(self._h, int(k0), int(nk), int(s), ctypes.byref(lo),
+                                   ctypes.byref(hi)))
+        return lo.value, hi.value
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _dev_f32(t, name):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda:
+        raise TypeError(f"{name} must be a float32 CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def ifdk_filter(g: Geometry, raw, filtered, v0: int = 0, stream=None) -> None:
+    """filtered = Alg. alg:filter(raw) for rows v0.. of each view; tensors [n_views][n_rows][Nu]."""
+    if tuple(raw.shape) != tuple(filtered.shape) or raw.dim() != 3 or raw.shape[2] != g.Nu:
+        raise ValueError("raw and filtered must both be [n_views][n_rows][Nu]")
+    _check(_lib.ifdk_filter(g.handle, _dev_f32(raw, "raw"), _dev_f32(filtered, "filtered"),
+                            raw.shape[0], int(v0), raw.shape[1], _stream_ptr(stream)))
+
+
+def ifdk_backproject(g: Geometry, filtered, s0: int, vol, k0: int = 0, v0: int = 0,
+                     accumulate: bool = False, stream=None) -> None:
+    """vol (=|+=) Alg. alg:bp over views s0..s0+n-1; filtered [n][n_rows][Nu] holds rows v0..,
+    vol [nk][Ny][Nx] is the slab k0..k0+nk-1."""
+    if filtered.dim() != 3 or filtered.shape[2] != g.Nu:
+        raise ValueError("filtered must be [n_views][n_rows][Nu]")
+    if vol.dim() != 3 or vol.shape[1] != g.Ny or vol.shape[2] != g.Nx:
+        raise ValueError("vol must be [nk][Ny][Nx]")
+    _check(_lib.ifdk_backproject(g.handle, _dev_f32(filtered, "filtered"), int(s0),
+                                 filtered.shape[0], int(v0), filtered.shape[1],
+                                 _dev_f32(vol, "vol"), int(k0), vol.shape[0],
+                                 1 if accumulate else 0, _stream_ptr(stream)))
+
+
+def ifdk_reconstruct(g: Geometry, raw, vol, stream=None) -> None:
+    """vol = FDK(raw): raw [n_views][Nv][Nu] device, vol [Nz][Ny][Nx] device."""
+    if raw.dim() != 3 or raw.shape[1] != g.Nv or raw.shape[2] != g.Nu:
+        raise ValueError("raw must be [n_views][Nv][Nu]")
+    if tuple(vol.shape) != (g.Nz, g.Ny, g.Nx):
+        raise ValueError("vol must be [Nz][Ny][Nx]")
+    _check(_lib.ifdk_reconstruct(g.handle, _dev_f32(raw, "raw"), raw.shape[0],
+                                 _dev_f32(vol, "vol"), _stream_ptr(stream)))
+
+
+def _host_f32(a, name):
+    import torch
+
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda or a.dtype != torch.float32 or not a.is_contiguous():
+            raise TypeError(f"{name} must be a contiguous float32 host tensor")
+        return a.data_ptr(), tuple(a.shape)
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous:
+        raise TypeError(f"{name} must be a C-contiguous float32 array")
+    return a.ctypes.data, a.shape
+
+
+def ifdk_reconstruct_host(g: Geometry, raw_host, vol_host, stream=None) -> None:
+    """End-to-end FDK from host memory (H2D, filter, back-project, D2H); synchronous."""
+    rp, rs = _host_f32(raw_host, "raw_host")
+    vp, vs = _host_f32(vol_host, "vol_host")
+    if len(rs) != 3 or rs[1] != g.Nv or rs[2] != g.Nu:
+        raise ValueError("raw_host must be [n_views][Nv][Nu]")
+    if tuple(vs) != (g.Nz, g.Ny, g.Nx):
+        raise ValueError("vol_host must be [Nz][Ny][Nx]")
+    _check(_lib.ifdk_reconstruct_host(g.handle, rp, rs[0], vp, _stream_ptr(stream)))

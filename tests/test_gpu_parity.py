@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 oracle, element by element,
+on the same seeded inputs (sizes the oracle finishes in seconds; several tiles and
+ragged tails), plus edge cases and bitwise invariants."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity_util import Q_MAX_REL, Q_RMSE, VOL_MAX_REL, VOL_RMSE, assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _spec(Np, Nu, Nv, Nx, Ny, Nz, **kw):
+    return synth.ConfigSpec(f"{Np}x{Nu}x{Nv}->{Nx}x{Ny}x{Nz}", Np, Nu, Nv, Nx, Ny, Nz, **kw)
+
+
+def _phantom_E(spec, s0=0, n=None, v0=0, n_rows=None):
+    n = spec.Np if n is None else n
+    ell = synth.default_ellipsoids(spec)
+    return synth.project(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta, ell, s0,
+                         n, v0, n_rows)
+
+
+def _oracle_Q32(spec, E, v0=0):
+    """Filtered views computed by the oracle, rounded to fp32: a seeded BP input that never
+    touches the CUDA path."""
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    return oracle.filter_fft(og, E, v0=v0).astype(np.float32)
+
+
+# ------------------------------------------------------------------------------- filter
+@pytest.mark.parametrize("Nu,n_rows,n_views,v0", [
+    (64, 64, 5, 0),      # odd number of rows overall: the last complex pair is half empty
+    (100, 30, 3, 7),     # Nu not a power of two: L = 256
+    (37, 5, 1, 0),       # odd Nu, a single view
+    (512, 8, 4, 200),    # a row band in the middle of the detector
+    (2048, 3, 2, 1000),  # L = 4096, the config-4/5 row length
+])
+def test_filter_matches_oracle(torch_cuda, Nu, n_rows, n_views, v0):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_filter
+
+    Nv = max(v0 + n_rows + 3, 16)
+    spec = _spec(90, Nu, Nv, 32, 32, 32)
+    g = Geometry.from_spec(spec)
+    rng = np.random.default_rng(Nu + n_rows)
+    E = (np.abs(rng.standard_normal((n_views, n_rows, Nu))) * 20).astype(np.float32)
+    raw = torch.from_numpy(E).cuda()
+    out = torch.empty_like(raw)
+    ifdk_filter(g, raw, out, v0=v0)
+    Qref = oracle.filter_direct(oracle.OracleGeometry(**spec.geometry_args()), E, v0=v0)
+    assert_parity(out.cpu().numpy(), Qref, Q_RMSE, Q_MAX_REL, "filter")
+    # in place
+    ifdk_filter(g, raw, raw, v0=v0)
+    assert torch.equal(raw, out)
+
+
+def test_filter_phantom_config1(torch_cuda):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_filter
+
+    spec = synth.config(1)
+    E = _phantom_E(spec)
+    raw = torch.from_numpy(E).cuda()
+    out = torch.empty_like(raw)
+    ifdk_filter(Geometry.from_spec(spec), raw, out)
+    Qref = oracle.filter_direct(oracle.OracleGeometry(**spec.geometry_args()), E)
+    assert_parity(out.cpu().numpy(), Qref, Q_RMSE, Q_MAX_REL, "filter config 1")
+
+
+# ------------------------------------------------------------------------------- back-projection
+def _bp_case(torch, spec, s0, n, k0, nk, v0=None, n_rows=None, accumulate_base=None, E=None):
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    g = Geometry.from_spec(spec)
+    if v0 is None:
+        v0, n_rows = 0, spec.Nv
+    if E is None:
+        E = _phantom_E(spec, s0, n, v0, n_rows)
+    Q = _oracle_Q32(spec, E, v0)
+    vol = torch.zeros((nk, spec.Ny, spec.Nx), device="cuda", dtype=torch.float32)
+    if accumulate_base is not None:
+        vol.copy_(torch.from_numpy(accumulate_base))
+    ifdk_backproject(g, torch.from_numpy(Q).cuda(), s0, vol, k0=k0, v0=v0,
+                     accumulate=accumulate_base is not None)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.backproject_volume(og, Q.astype(np.float64), s0=s0, v0=v0, k0=k0, nk=nk)
+    if accumulate_base is not None:
+        ref = ref + accumulate_base
+    return vol.cpu().numpy(), ref
+
+
+def test_bp_config1_full_volume(torch_cuda):
+    got, ref = _bp_case(torch_cuda, synth.config(1), 0, 64, 0, 64)
+    assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL, "bp config 1")
+
+
+def test_bp_ragged_tiles_slab_band_and_accumulate(torch_cuda):
+    """Nx, Ny not multiples of the 16x16 tile, Nz not a multiple of the 64-slice chunk, an
+    unaligned slab, a view offset and a detector row band; accumulate into a non-zero slab."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry
+
+    spec = _spec(150, 80, 72, 37, 23, 150)
+    g = Geometry.from_spec(spec)
+    s0, n, k0, nk = 17, 29, 45, 90
+    lo = min(g.band_rows(k0, nk, s)[0] for s in range(s0, s0 + n))
+    hi = max(g.band_rows(k0, nk, s)[1] for s in range(s0, s0 + n))
+    base = np.random.default_rng(3).standard_normal((nk, spec.Ny, spec.Nx)).astype(np.float32)
+    got, ref = _bp_case(torch, spec, s0, n, k0, nk, v0=lo, n_rows=hi - lo + 1, accumulate_base=base)
+    assert_parity(got - base, ref - base, VOL_RMSE, VOL_MAX_REL, "bp ragged")
+
+
+def test_bp_truncated_detector_zero_border(torch_cuda):
+    """A detector smaller than the volume's shadow: taps off the detector read 0 (c-A9)."""
+    spec = _spec(40, 24, 20, 32, 32, 40, det_mm=120.0)
+    got, ref = _bp_case(torch_cuda, spec, 0, 40, 0, 40)
+    assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL, "bp truncated")
+
+
+def test_bp_global_path_nu_not_multiple_of_4(torch_cuda):
+    """Nu % 4 != 0 cannot be described to TMA; the kernel reads taps from global memory."""
+    spec = _spec(45, 30, 34, 20, 20, 20)
+    got, ref = _bp_case(torch_cuda, spec, 3, 45, 0, 20)
+    assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL, "bp global path")
+
+
+def test_bp_slab_split_is_bitwise_and_deterministic(torch_cuda):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    spec = _spec(48, 96, 96, 48, 40, 200)
+    g = Geometry.from_spec(spec)
+    Q = torch.from_numpy(_oracle_Q32(spec, _phantom_E(spec))).cuda()
+    full = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+    ifdk_backproject(g, Q, 0, full)
+    again = torch.empty_like(full)
+    ifdk_backproject(g, Q, 0, again)
+    assert torch.equal(full, again)
+    for cuts in ((0, 64, 200), (0, 77, 131, 200), (0, 1, 199, 200)):
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            slab = torch.empty((b - a, spec.Ny, spec.Nx), device="cuda")
+            lo = min(g.band_rows(a, b - a, s)[0] for s in range(spec.Np))
+            hi = max(g.band_rows(a, b - a, s)[1] for s in range(spec.Np))
+            ifdk_backproject(g, Q[:, lo:hi + 1].contiguous(), 0, slab, k0=a, v0=lo)
+            assert torch.equal(slab, full[a:b]), (cuts, a, b)
+
+
+def test_bp_view_split_accumulate_matches(torch_cuda):
+    """Views in two calls (accumulate) vs one call: equal up to fp32 summation order."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    spec = _spec(64, 64, 64, 40, 40, 40)
+    g = Geometry.from_spec(spec)
+    Q = torch.from_numpy(_oracle_Q32(spec, _phantom_E(spec))).cuda()
+    one = torch.empty((40, 40, 40), device="cuda")
+    ifdk_backproject(g, Q, 0, one)
+    two = torch.empty_like(one)
+    ifdk_backproject(g, Q[:30].contiguous(), 0, two)
+    ifdk_backproject(g, Q[30:].contiguous(), 30, two, accumulate=True)
+    assert_parity(two.cpu().numpy(), one.cpu().numpy(), 1e-6, 1e-5, "view split")
+
+
+def test_bp_band_not_covering_is_shape_error(torch_cuda):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, IfdkError, ifdk_backproject
+
+    spec = _spec(16, 64, 64, 32, 32, 32)
+    g = Geometry.from_spec(spec)
+    Q = torch.zeros((16, 10, 64), device="cuda")
+    vol = torch.zeros((32, 32, 32), device="cuda")
+    with pytest.raises(IfdkError) as e:
+        ifdk_backproject(g, Q, 0, vol, v0=27)
+    assert e.value.status == 3
+
+
+def test_bp_zero_views(torch_cuda):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    spec = _spec(16, 64, 64, 32, 32, 32)
+    g = Geometry.from_spec(spec)
+    vol = torch.ones((32, 32, 32), device="cuda")
+    ifdk_backproject(g, torch.zeros((0, 64, 64), device="cuda"), 0, vol, accumulate=True)
+    assert torch.all(vol == 1)
+    ifdk_backproject(g, torch.zeros((0, 64, 64), device="cuda"), 0, vol)
+    assert torch.all(vol == 0)
+
+
+# ------------------------------------------------------------------------------- whole FDK
+def test_reconstruct_config1(torch_cuda):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_reconstruct
+
+    spec = synth.config(1)
+    E = _phantom_E(spec)
+    vol = torch.empty((64, 64, 64), device="cuda")
+    ifdk_reconstruct(Geometry.from_spec(spec), torch.from_numpy(E).cuda(), vol)
+    ref = oracle.reconstruct(oracle.OracleGeometry(**spec.geometry_args()), E)
+    assert_parity(vol.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "reconstruct config 1")
+
+
+def test_reconstruct_noisy_stress_input(torch_cuda):
+    """E + N(0, (0.01 max E)^2): roughens Q and stresses the coordinate numerics."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_reconstruct
+
+    spec = _spec(96, 128, 128, 96, 96, 96)
+    E = _phantom_E(spec)
+    E = synth.add_noise(E, 0.01 * float(E.max()), seed=1234)
+    vol = torch.empty((96, 96, 96), device="cuda")
+    ifdk_reconstruct(Geometry.from_spec(spec), torch.from_numpy(E).cuda(), vol)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.reconstruct(og, E, fft=True)
+    assert_parity(vol.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "reconstruct noisy")
+
+
+def test_reconstruct_host_equals_device(torch_cuda):
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_reconstruct, ifdk_reconstruct_host
+
+    spec = _spec(300, 64, 64, 48, 48, 48)  # > one 256-view batch
+    g = Geometry.from_spec(spec)
+    E = _phantom_E(spec)
+    vol_d = torch.empty((48, 48, 48), device="cuda")
+    ifdk_reconstruct(g, torch.from_numpy(E).cuda(), vol_d)
+    vol_h = np.empty((48, 48, 48), np.float32)
+    ifdk_reconstruct_host(g, E, vol_h)
+    assert np.array_equal(vol_h, vol_d.cpu().numpy())
+
+
+def test_synth_gpu_generator_matches_cpu(torch_cuda):
+    torch = torch_cuda
+    spec = synth.config(2)
+    ell = synth.default_ellipsoids(spec)
+    args = (spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta, ell)
+    out = torch.empty((3, 512, 512), device="cuda")
+    synth.project_gpu(*args, 100, 3, 0, 512, out.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = synth.project(*args, 100, 3)
+    assert np.max(np.abs(out.cpu().numpy() - ref)) <= 1e-5 * ref.max()
