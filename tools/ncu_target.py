@@ -1,0 +1,23 @@
+"""One filter launch + one BP launch on a config's first views (ncu capture target)."""
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+import synth  # noqa: E402
+from paper_1909_02724_b200 import Geometry, ifdk_backproject, ifdk_filter  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+spec = synth.config(cfg)
+g = Geometry.from_spec(spec)
+E = torch.empty((n, spec.Nv, spec.Nu), device="cuda")
+synth.project_gpu(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta,
+                  synth.default_ellipsoids(spec), 0, n, 0, spec.Nv, E.data_ptr(),
+                  torch.cuda.current_stream().cuda_stream)
+Q = torch.empty_like(E)
+vol = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+ifdk_filter(g, E, Q)
+ifdk_backproject(g, Q, 0, vol)
+torch.cuda.synchronize()
+print("done", float(vol.abs().max()))
