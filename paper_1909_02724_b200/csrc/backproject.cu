@@ -55,7 +55,10 @@ struct BPParams {
 
 struct __align__(16) Meta {
     double P[10];
-    int u_org, v_org, fast, pad;
+    int u_org, v_org;    // box origin (detector column, row)
+    int w_need, h_need;  // columns / rows of the box the tile x chunk can touch
+    int fast;            // the patch fits the box
+    int pad[3];
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p)
@@ -272,6 +275,8 @@ __device__ void compute_meta(Meta* m, const BPParams& p, long t, int i_lo, int i
                    fv0 > -1e9 && fv1 < 1e9)
                       ? 1
                       : 0;
+        m->w_need = m->fast ? (int)w_need : 0;
+        m->h_need = m->fast ? (int)h_need : 0;
     }
 }
 
@@ -319,17 +324,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                         meta[t & 3].v_org - p.v0, (int)t);
         }
     };
-    auto transform = [&](long t) {  // all threads: raw box -> (a, delta) pairs
+    auto transform = [&](long t) {  // all threads: used part of the raw box -> (a, delta) pairs
         const Meta& m = meta[t & 3];
         if (!m.fast) return;
         const float* r = reinterpret_cast<const float*>(raw_of(t));
         float2* q = pair_of(t);
-        const int wp = p.box_w - 1, total = p.box_h * wp;
-        for (int e = tid; e < total; e += kThreads) {
-            const int rr = e / wp, cc = e - rr * wp;
-            const float a = r[rr * p.box_w + cc], b = r[rr * p.box_w + cc + 1];
-            q[rr * P2 + cc] = make_float2(a, b - a);
-        }
+        const int wp = m.w_need - 1, hn = m.h_need;
+        for (int rr = warp; rr < hn; rr += kThreads / 32)  // one detector row per warp
+            for (int cc = lane; cc < wp; cc += 32) {
+                const float a = r[rr * p.box_w + cc], b = r[rr * p.box_w + cc + 1];
+                q[rr * P2 + cc] = make_float2(a, b - a);
+            }
     };
 
     if (TMA) {

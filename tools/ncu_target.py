@@ -9,6 +9,7 @@ from paper_1909_02724_b200 import Geometry, ifdk_backproject, ifdk_filter  # noq
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+nk = int(sys.argv[3]) if len(sys.argv) > 3 else None
 spec = synth.config(cfg)
 g = Geometry.from_spec(spec)
 E = torch.empty((n, spec.Nv, spec.Nu), device="cuda")
@@ -16,8 +17,10 @@ synth.project_gpu(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta
                   synth.default_ellipsoids(spec), 0, n, 0, spec.Nv, E.data_ptr(),
                   torch.cuda.current_stream().cuda_stream)
 Q = torch.empty_like(E)
-vol = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+nk = nk or spec.Nz
+k0 = (spec.Nz - nk) // 2 // 64 * 64
+vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
 ifdk_filter(g, E, Q)
-ifdk_backproject(g, Q, 0, vol)
+ifdk_backproject(g, Q, 0, vol, k0=k0)
 torch.cuda.synchronize()
 print("done", float(vol.abs().max()))
