@@ -24,6 +24,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -33,7 +34,6 @@ namespace ifdk {
 namespace {
 
 constexpr int kTI = 16, kTJ = 16, kThreads = 256;
-constexpr int kKC = 64;
 
 struct BPParams {
     const double* P;  // [n_views][10]: P00 P01 P03 | P10 P11 P12 P13 | P20 P21 P23
@@ -239,22 +239,35 @@ __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i
     }
 }
 
-// Patch box of view t for the tile (warp 0): corners of the tile, both ends of the chunk.
-__device__ void compute_meta(Meta* m, const BPParams& p, long t, int i_lo, int i_hi, int j_lo,
-                             int j_hi, int kb, int kv0, int kv1)
+// Patch boxes of views t0 .. t0+7 for the tile, computed by warp 0 in one pass: lane l takes
+// view t0 + l/4 and corner l%4 of the tile (u, v are linear-fractional in the column position,
+// so the extremes over the tile sit at its corners), at both ends of the chunk; min/max over
+// the 4 lanes of a view.  One pass per 8 views keeps warp 0 from straggling at the barrier.
+constexpr int kMetaRing = 16;
+
+__device__ void compute_meta8(Meta* ring, const BPParams& p, long t0, int i_lo, int i_hi,
+                              int j_lo, int j_hi, int kb, int kv0, int kv1)
 {
     const int lane = threadIdx.x & 31;
-    const double* Pg = p.P + t * 10;
-    if (lane < 10) m->P[lane] = Pg[lane];
     const int corner = lane & 3;
-    const double ci = (corner & 1) ? i_hi : i_lo;
-    const double cj = (corner & 2) ? j_hi : j_lo;
+    const long t_raw = t0 + (lane >> 2);
+    const bool valid = t_raw < p.n_views;
+    const long t = valid ? t_raw : p.n_views - 1;
+    const double* Pg = p.P + t * 10;
     double P[10];
 #pragma unroll
     for (int q = 0; q < 10; ++q) P[q] = __ldg(Pg + q);
+    Meta* m = &ring[t_raw & (kMetaRing - 1)];
+    if (valid) {
+#pragma unroll
+        for (int q = 0; q < 10; ++q)
+            if ((q & 3) == corner) m->P[q] = P[q];  // static indices: no local-memory copy
+    }
+    const double ci = (corner & 1) ? i_hi : i_lo;
+    const double cj = (corner & 2) ? j_hi : j_lo;
     const ColInv c = column_invariants(P, ci, cj, (double)kb);
     double umin = c.u, umax = c.u;
-    double va = c.v + kv0 * c.dv, vb = c.v + (kv1 - 1) * c.dv;
+    const double va = c.v + kv0 * c.dv, vb = c.v + (kv1 - 1) * c.dv;
     double vmin = fmin(va, vb), vmax = fmax(va, vb);
 #pragma unroll
     for (int o = 1; o < 4; o <<= 1) {
@@ -263,25 +276,25 @@ __device__ void compute_meta(Meta* m, const BPParams& p, long t, int i_lo, int i
         vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
-    if (lane == 0) {
+    if (corner == 0 && valid) {
         const double fu0 = floor(umin), fu1 = floor(umax), fv0 = floor(vmin), fv1 = floor(vmax);
         // TMA (tile mode, no swizzle) faults unless the innermost box coordinate is a
         // multiple of 16 bytes (measured: tools/tma_probe.cu), so the column origin is
         // rounded down to a multiple of 4 floats.
-        m->u_org = ((int)fu0 - 1) & ~3;
-        m->v_org = (int)fv0 - 1;
-        const double w_need = fu1 + 3.0 - m->u_org, h_need = fv1 - fv0 + 4.0;
-        m->fast = (w_need <= p.box_w && h_need <= p.box_h && fu0 > -1e9 && fu1 < 1e9 &&
-                   fv0 > -1e9 && fv1 < 1e9)
-                      ? 1
-                      : 0;
-        m->w_need = m->fast ? (int)w_need : 0;
-        m->h_need = m->fast ? (int)h_need : 0;
+        const bool finite = fu0 > -1e9 && fu1 < 1e9 && fv0 > -1e9 && fv1 < 1e9;
+        const int u_org = finite ? (((int)fu0 - 1) & ~3) : 0;
+        const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0;
+        const bool fits = finite && w_need <= p.box_w && h_need <= p.box_h;
+        m->u_org = u_org;
+        m->v_org = finite ? (int)fv0 - 1 : 0;
+        m->fast = fits ? 1 : 0;
+        m->w_need = fits ? (int)w_need : 0;
+        m->h_need = fits ? (int)h_need : 0;
     }
 }
 
 template <int KC, int P2, bool TMA>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap)
 {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -306,8 +319,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     float2* const pair0 = reinterpret_cast<float2*>(smem + 2 * p.raw_bytes);
     auto raw_of = [&](long t) { return smem + (t & 1) * p.raw_bytes; };
     auto pair_of = [&](long t) { return pair0 + (t & 1) * p.box_h * P2; };
-    Meta* meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_h * P2);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(meta + 4);
+    Meta* meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_h * P2);  // ring of kMetaRing
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
     const uint32_t tx_bytes = (uint32_t)(p.box_w * p.box_h * 4);
 
     // The tensor map must be addressed in param space (__grid_constant__): take its address
@@ -315,17 +328,20 @@ __global__ void __launch_bounds__(kThreads, 2)
     // it to local memory, an illegal TMA operand).
     const CUtensorMap* const tmap_ptr = &tmap;
     auto issue = [=](long t) {  // warp 0 only
-        compute_meta(&meta[t & 3], p, t, i_lo, i_hi, j_lo, j_hi, kb, kv0, kv1);
-        __syncwarp();
+        if ((t & 7) == 0) {
+            compute_meta8(meta, p, t, i_lo, i_hi, j_lo, j_hi, kb, kv0, kv1);
+            __syncwarp();
+        }
         if (TMA && lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&mbar[t & 1], tx_bytes);
-            tma_load_3d(smem + (t & 1) * p.raw_bytes, tmap_ptr, &mbar[t & 1], meta[t & 3].u_org,
-                        meta[t & 3].v_org - p.v0, (int)t);
+            const Meta& m = meta[t & (kMetaRing - 1)];
+            tma_load_3d(smem + (t & 1) * p.raw_bytes, tmap_ptr, &mbar[t & 1], m.u_org,
+                        m.v_org - p.v0, (int)t);
         }
     };
     auto transform = [&](long t) {  // all threads: used part of the raw box -> (a, delta) pairs
-        const Meta& m = meta[t & 3];
+        const Meta& m = meta[t & (kMetaRing - 1)];
         if (!m.fast) return;
         const float* r = reinterpret_cast<const float*>(raw_of(t));
         float2* q = pair_of(t);
@@ -357,11 +373,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (warp == 0 && n > 2) issue(2);
     }
 
+    // first view after which the partial sums are flushed: s0 + t + 1 = 0 (mod vb)
+    long next_flush = p.vb - 1 - (p.s0 % p.vb + p.vb) % p.vb;
     for (long t = 0; t < n; ++t) {
         const double* P;
         int u_org = 0, v_org = 0, fast = 0;
         if (TMA) {
-            const Meta& m = meta[t & 3];
+            const Meta& m = meta[t & (kMetaRing - 1)];
             P = m.P;
             u_org = m.u_org;
             v_org = m.v_org;
@@ -385,11 +403,12 @@ __global__ void __launch_bounds__(kThreads, 2)
             } else {
                 accumulate_view_global<KC>(acc, p.Q + t * (long)p.n_rows * p.Nu, p, ti, kv0, kv1);
             }
-            if ((p.s0 + t + 1) % p.vb == 0 || t == n - 1) {
+            if (t == next_flush || t == n - 1) {
                 flush<KC>(acc, p, i, j, kb, kv0, kv1, overwrite);
                 overwrite = false;
             }
         }
+        if (t == next_flush) next_flush += p.vb;
         if (TMA) {
             if (t + 1 < n) {
                 mbar_wait(&mbar[(t + 1) & 1], (uint32_t)(((t + 1) >> 1) & 1));
@@ -415,24 +434,36 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
-template <int P2>
+template <int KC, int P2>
 ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, bool tma, dim3 grid, size_t smem,
                      cudaStream_t st)
 {
     cudaError_t e;
     if (tma) {
-        auto k = bp_kernel<kKC, P2, true>;
+        auto k = bp_kernel<KC, P2, true>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp)");
         k<<<grid, kThreads, smem, st>>>(p, map);
     } else {
-        auto k = bp_kernel<kKC, P2, false>;
+        auto k = bp_kernel<KC, P2, false>;
         k<<<grid, kThreads, 0, st>>>(p, map);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "bp_kernel launch");
     count_launch();
     return IFDK_OK;
+}
+
+// Slices per k-chunk (= register accumulators per thread).  The choice depends on the geometry
+// only, never on the slab, so every decomposition of a volume walks identical chunks.
+int choose_kc(const ifdk_geometry* g)
+{
+    if (const char* e = std::getenv("IFDK_BP_KC")) {
+        const int v = std::atoi(e);
+        if (v == 32 || v == 64) return v;
+    }
+    (void)g;
+    return 32;  // measured on B200, config 3/4: 32 slices (3 CTAs/SM) beat 64 (2 CTAs/SM) by 10%
 }
 
 }  // namespace
@@ -474,16 +505,17 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     p.Nu = g->Nu; p.Nv = g->Nv; p.Nx = g->Nx; p.Ny = g->Ny;
     p.v0 = v0; p.n_rows = n_rows;
     p.k0 = k0; p.nk = nk;
-    p.kb0 = (k0 / kKC) * kKC;
+    const int KC = choose_kc(g);
+    p.kb0 = (k0 / KC) * KC;
     p.tiles_i = (g->Nx + kTI - 1) / kTI;
     const int tiles_j = (g->Ny + kTJ - 1) / kTJ;
-    const int n_chunks = (k0 + nk - p.kb0 + kKC - 1) / kKC;
+    const int n_chunks = (k0 + nk - p.kb0 + KC - 1) / KC;
     p.vb = 128;
     p.accumulate = accumulate;
 
     // Box of the staged patch from the conservative geometric bound.
     double wb, hb;
-    patch_bound(g, kTI, kTJ, kKC, &wb, &hb);
+    patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
     int box_h = (int)std::ceil(hb) + 6;
     if (box_w < 8) box_w = 8;
@@ -499,7 +531,7 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
         p.box_w = box_w;
         p.box_h = box_h;
         p.raw_bytes = (box_w * box_h * 4 + 127) / 128 * 128;
-        smem = 2 * (size_t)p.raw_bytes + 2 * sizeof(float2) * box_h * P2 + 4 * sizeof(Meta) + 16;
+        smem = 2 * (size_t)p.raw_bytes + 2 * sizeof(float2) * box_h * P2 + kMetaRing * sizeof(Meta) + 16;
         cuuint64_t dims[3] = {(cuuint64_t)g->Nu, (cuuint64_t)n_rows, (cuuint64_t)n_views};
         cuuint64_t strides[2] = {(cuuint64_t)g->Nu * 4, (cuuint64_t)g->Nu * 4 * n_rows};
         cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
@@ -518,11 +550,20 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
     dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
     ifdk_status s;
-    switch (P2) {
-        case 24: s = launch_t<24>(p, map, tma, grid, smem, st); break;
-        case 40: s = launch_t<40>(p, map, tma, grid, smem, st); break;
-        case 56: s = launch_t<56>(p, map, tma, grid, smem, st); break;
-        default: s = launch_t<72>(p, map, tma, grid, smem, st); break;
+    if (KC == 32) {
+        switch (P2) {
+            case 24: s = launch_t<32, 24>(p, map, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40>(p, map, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56>(p, map, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72>(p, map, tma, grid, smem, st); break;
+        }
+    } else {
+        switch (P2) {
+            case 24: s = launch_t<64, 24>(p, map, tma, grid, smem, st); break;
+            case 40: s = launch_t<64, 40>(p, map, tma, grid, smem, st); break;
+            case 56: s = launch_t<64, 56>(p, map, tma, grid, smem, st); break;
+            default: s = launch_t<64, 72>(p, map, tma, grid, smem, st); break;
+        }
     }
     cudaFreeAsync(Pd, st);
     return s;
