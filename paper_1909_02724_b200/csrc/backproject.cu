@@ -239,30 +239,23 @@ __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i
     }
 }
 
-// Patch boxes of views t0 .. t0+7 for the tile, computed by warp 0 in one pass: lane l takes
-// view t0 + l/4 and corner l%4 of the tile (u, v are linear-fractional in the column position,
-// so the extremes over the tile sit at its corners), at both ends of the chunk; min/max over
-// the 4 lanes of a view.  One pass per 8 views keeps warp 0 from straggling at the barrier.
+// Patch box of view t for the tile, computed by one warp: lane l takes corner l%4 of the
+// tile (u, v are linear-fractional in the column position, so the extremes over the tile sit
+// at its corners) at both ends of the chunk; min/max over the 4 corners.  Every 8 views the
+// 8 warps compute the boxes of the next 8 views together, so no warp straggles at the barrier.
 constexpr int kMetaRing = 16;
 
-__device__ void compute_meta8(Meta* ring, const BPParams& p, long t0, int i_lo, int i_hi,
-                              int j_lo, int j_hi, int kb, int kv0, int kv1)
+__device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, int i_hi, int j_lo,
+                              int j_hi, int kb, int kv0, int kv1)
 {
     const int lane = threadIdx.x & 31;
     const int corner = lane & 3;
-    const long t_raw = t0 + (lane >> 2);
-    const bool valid = t_raw < p.n_views;
-    const long t = valid ? t_raw : p.n_views - 1;
-    const double* Pg = p.P + t * 10;
+    const double* Pg = p.P + (long)t * 10;
     double P[10];
 #pragma unroll
     for (int q = 0; q < 10; ++q) P[q] = __ldg(Pg + q);
-    Meta* m = &ring[t_raw & (kMetaRing - 1)];
-    if (valid) {
-#pragma unroll
-        for (int q = 0; q < 10; ++q)
-            if ((q & 3) == corner) m->P[q] = P[q];  // static indices: no local-memory copy
-    }
+    Meta* m = &ring[t & (kMetaRing - 1)];
+    if (lane < 10) m->P[lane] = __ldg(Pg + lane);
     const double ci = (corner & 1) ? i_hi : i_lo;
     const double cj = (corner & 2) ? j_hi : j_lo;
     const ColInv c = column_invariants(P, ci, cj, (double)kb);
@@ -276,7 +269,7 @@ __device__ void compute_meta8(Meta* ring, const BPParams& p, long t0, int i_lo, 
         vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
-    if (corner == 0 && valid) {
+    if (lane == 0) {
         const double fu0 = floor(umin), fu1 = floor(umax), fv0 = floor(vmin), fv1 = floor(vmax);
         // TMA (tile mode, no swizzle) faults unless the innermost box coordinate is a
         // multiple of 16 bytes (measured: tools/tma_probe.cu), so the column origin is
@@ -303,9 +296,13 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
     const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
     const bool active = i < p.Nx && j < p.Ny;
+    // Columns past the volume edge shadow the last valid column (branch-free update loop);
+    // they never write.
+    const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
     const int i_lo = tile_i * kTI, i_hi = min(i_lo + kTI, p.Nx) - 1;
     const int j_lo = tile_j * kTJ, j_hi = min(j_lo + kTJ, p.Ny) - 1;
     const int kb = p.kb0 + (int)blockIdx.y * KC;
+    const double dkb = (double)kb;
     const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, KC);
     const bool full = kv0 == 0 && kv1 == KC;
 
@@ -313,44 +310,43 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) acc[kk] = 0.f;
     bool overwrite = !p.accumulate;
-    const long n = p.n_views;
+    const int n = (int)p.n_views;
 
     // raw box of view t: smem + (t & 1) raw_bytes; pair patch of view t: pair0 + (t & 1) box_h P2
     float2* const pair0 = reinterpret_cast<float2*>(smem + 2 * p.raw_bytes);
-    auto raw_of = [&](long t) { return smem + (t & 1) * p.raw_bytes; };
-    auto pair_of = [&](long t) { return pair0 + (t & 1) * p.box_h * P2; };
-    Meta* meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_h * P2);  // ring of kMetaRing
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
+    Meta* const meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_h * P2);  // ring of kMetaRing
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
     const uint32_t tx_bytes = (uint32_t)(p.box_w * p.box_h * 4);
-
     // The tensor map must be addressed in param space (__grid_constant__): take its address
     // here, in the kernel body, never through a by-reference lambda capture (which would copy
     // it to local memory, an illegal TMA operand).
     const CUtensorMap* const tmap_ptr = &tmap;
-    auto issue = [=](long t) {  // warp 0 only
-        if ((t & 7) == 0) {
-            compute_meta8(meta, p, t, i_lo, i_hi, j_lo, j_hi, kb, kv0, kv1);
-            __syncwarp();
-        }
-        if (TMA && lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_expect_tx(&mbar[t & 1], tx_bytes);
-            const Meta& m = meta[t & (kMetaRing - 1)];
-            tma_load_3d(smem + (t & 1) * p.raw_bytes, tmap_ptr, &mbar[t & 1], m.u_org,
-                        m.v_org - p.v0, (int)t);
+
+    auto issue = [=](int t) {  // one thread: TMA of view t's box into raw buffer t & 1
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[t & 1], tx_bytes);
+        tma_load_3d(smem + (t & 1) * p.raw_bytes, tmap_ptr, &mbar[t & 1], m.u_org, m.v_org - p.v0,
+                    t);
+    };
+    auto transform = [=](int t) {  // all threads: used part of the raw box -> (a, b - a) pairs
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        const float* r = reinterpret_cast<const float*>(smem + (t & 1) * p.raw_bytes);
+        float2* q = pair0 + (t & 1) * p.box_h * P2;
+        const int wp = m.w_need - 1, hn = m.h_need;
+        for (int rr = warp; rr < hn; rr += kThreads / 32) {  // one detector row per warp
+            const float* rrow = r + rr * p.box_w;
+            for (int c0 = 0; c0 < wp; c0 += 32) {
+                const int cc = c0 + lane;
+                const float a = cc < p.box_w ? rrow[cc] : 0.f;
+                float b = __shfl_down_sync(0xffffffffu, a, 1);
+                if (lane == 31 && cc + 1 < p.box_w) b = rrow[cc + 1];
+                if (cc < wp) q[rr * P2 + cc] = make_float2(a, b - a);
+            }
         }
     };
-    auto transform = [&](long t) {  // all threads: used part of the raw box -> (a, delta) pairs
-        const Meta& m = meta[t & (kMetaRing - 1)];
-        if (!m.fast) return;
-        const float* r = reinterpret_cast<const float*>(raw_of(t));
-        float2* q = pair_of(t);
-        const int wp = m.w_need - 1, hn = m.h_need;
-        for (int rr = warp; rr < hn; rr += kThreads / 32)  // one detector row per warp
-            for (int cc = lane; cc < wp; cc += 32) {
-                const float a = r[rr * p.box_w + cc], b = r[rr * p.box_w + cc + 1];
-                q[rr * P2 + cc] = make_float2(a, b - a);
-            }
+    auto metas = [=](int t0) {  // all warps: boxes of views t0 .. t0+7
+        if (t0 + warp < n) compute_meta1(meta, p, t0 + warp, i_lo, i_hi, j_lo, j_hi, kb, kv0, kv1);
     };
 
     if (TMA) {
@@ -359,63 +355,65 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
             mbar_init(&mbar[1], 1);
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
+        metas(0);
         __syncthreads();
-        if (warp == 0) {
+        if (tid == 0) {
             if (n > 0) issue(0);
             if (n > 1) issue(1);
         }
-        __syncthreads();
         if (n > 0) {
             mbar_wait(&mbar[0], 0);
+            if (!meta[0].fast) __trap();  // the host sizes the box from a conservative bound
             transform(0);
         }
         __syncthreads();
-        if (warp == 0 && n > 2) issue(2);
+        if (tid == 0 && n > 2) issue(2);
     }
 
     // first view after which the partial sums are flushed: s0 + t + 1 = 0 (mod vb)
-    long next_flush = p.vb - 1 - (p.s0 % p.vb + p.vb) % p.vb;
-    for (long t = 0; t < n; ++t) {
-        const double* P;
-        int u_org = 0, v_org = 0, fast = 0;
+    int next_flush = (int)(p.vb - 1 - (p.s0 % p.vb + p.vb) % p.vb);
+    for (int t = 0; t < n; ++t) {
+        double Pr[10];
+        int u_org = 0, v_org = 0;
         if (TMA) {
             const Meta& m = meta[t & (kMetaRing - 1)];
-            P = m.P;
+            const double2* P2v = reinterpret_cast<const double2*>(m.P);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const double2 d = P2v[q];
+                Pr[2 * q] = d.x;
+                Pr[2 * q + 1] = d.y;
+            }
             u_org = m.u_org;
             v_org = m.v_org;
-            fast = m.fast;
         } else {
-            P = p.P + t * 10;
-        }
-        if (active) {
-            double Pr[10];
 #pragma unroll
-            for (int q = 0; q < 10; ++q) Pr[q] = P[q];
-            const ThreadInv ti = split(column_invariants(Pr, (double)i, (double)j, (double)kb));
-            if constexpr (TMA) {
-                // The host sizes the box from a conservative bound, so every view fits.
-                if (!fast) __trap();
-                const uint32_t pb = smem_u32(pair_of(t));
-                if (full)
-                    accumulate_view_smem<KC, P2, true>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
-                else
-                    accumulate_view_smem<KC, P2, false>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
-            } else {
-                accumulate_view_global<KC>(acc, p.Q + t * (long)p.n_rows * p.Nu, p, ti, kv0, kv1);
-            }
-            if (t == next_flush || t == n - 1) {
-                flush<KC>(acc, p, i, j, kb, kv0, kv1, overwrite);
-                overwrite = false;
-            }
+            for (int q = 0; q < 10; ++q) Pr[q] = __ldg(p.P + (long)t * 10 + q);
         }
-        if (t == next_flush) next_flush += p.vb;
+        const ThreadInv ti = split(column_invariants(Pr, di, dj, dkb));
+        if constexpr (TMA) {
+            const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
+            if (full)
+                accumulate_view_smem<KC, P2, true>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
+            else
+                accumulate_view_smem<KC, P2, false>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
+        } else {
+            accumulate_view_global<KC>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0, kv1);
+        }
+        if (t == next_flush || t == n - 1) {
+            if (active) flush<KC>(acc, p, i, j, kb, kv0, kv1, overwrite);
+            overwrite = false;
+            next_flush += p.vb;
+        }
         if (TMA) {
             if (t + 1 < n) {
                 mbar_wait(&mbar[(t + 1) & 1], (uint32_t)(((t + 1) >> 1) & 1));
+                if (!meta[(t + 1) & (kMetaRing - 1)].fast) __trap();
                 transform(t + 1);
             }
+            if (((t + 3) & 7) == 0) metas(t + 3);
             __syncthreads();
-            if (warp == 0 && t + 3 < n) issue(t + 3);
+            if (tid == 0 && t + 3 < n) issue(t + 3);
         }
     }
 }
