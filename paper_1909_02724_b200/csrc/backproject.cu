@@ -50,6 +50,7 @@ struct BPParams {
     int raw_bytes;    // bytes of one raw box (multiple of 128)
     int vb;           // view batch of the two-level summation
     uint32_t neg_magic;  // -0x4B000000 * P2 * 8 mod 2^32 (see accumulate_view_smem)
+    int pair;            // PAIR walk (dv < 1 everywhere)
     int accumulate;
 };
 
@@ -159,33 +160,65 @@ __device__ __forceinline__ uint32_t floor_bits(float v, float* fr)
 }
 
 // One view from the (a, delta) pair patch in shared memory.
-template <int KC, int P2, bool FULL>
+//
+// PAIR (needs dv < 1 px per slice, true for every config): two consecutive slices kk, kk+1
+// touch at most three detector rows n, n+1, n+2 (v grows by dv < 1), so one floor, three
+// LDS.64 and three horizontal lerps serve both updates: slice kk+1 uses rows (n, n+1) or
+// (n+1, n+2) depending on whether fr + dv crosses 1.  12 B of shared memory per update
+// instead of 16.  The partial-chunk path runs the same arithmetic and only masks the
+// accumulation, so a slab split never changes a bit.
+template <int KC, int P2, bool FULL, bool PAIR>
 __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t pair_base,
                                                      uint32_t neg_magic, const ThreadInv& t,
                                                      int u_org, int v_org, int kv0, int kv1)
 {
     // byte address of pair (row nv + n, col nu) = pair_base + ((nv - v_org + n) P2 + nu - u_org) 8
     // neg_magic = -0x4B000000 * P2 * 8 (mod 2^32) arrives as a kernel parameter so that ptxas
-    // cannot split it back out of the base: one IMAD per update forms the tap address.
+    // cannot split it back out of the base: one IMAD per floor forms the tap address.
     const uint32_t a0 =
         pair_base + (uint32_t)(((t.nv - v_org) * P2 + (t.nu - u_org)) * 8) + neg_magic;
+    constexpr uint32_t S = P2 * 8;
     float fv0 = t.fv0;
+    if constexpr (PAIR) {
 #pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
-        // Every 8 updates, launder fv0 through a volatile asm so that the compiler cannot
-        // hoist the address arithmetic of later updates above earlier shared loads (which
-        // would need a register per hoisted address and spill the 64 accumulators).
-        if ((kk & 7) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
-        if (!FULL && (kk < kv0 || kk >= kv1)) continue;
-        float fr;
-        const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
-        const uint32_t addr = bits * (uint32_t)(P2 * 8) + a0;
-        const float2 p0 = lds64(addr);
-        const float2 p1 = lds64(addr + P2 * 8);
-        const float h0 = fmaf(t.du, p0.y, p0.x);
-        const float h1 = fmaf(t.du, p1.y, p1.x);
-        const float val = fmaf(fr, h1 - h0, h0);  // Alg. alg:subpixel lines 4-6
-        acc[kk] = fmaf(t.W, val, acc[kk]);        // I += W_dis . interp2, Alg. alg:bp line 10
+        for (int kk = 0; kk < KC; kk += 2) {
+            // Every 8 slices, launder fv0 through a volatile asm so that the compiler cannot
+            // hoist the address arithmetic of later slices above earlier shared loads.
+            if ((kk & 7) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            float fr0;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
+            const uint32_t addr = bits * S + a0;
+            const float2 p0 = lds64(addr);
+            const float2 p1 = lds64(addr + S);
+            const float2 p2 = lds64(addr + 2 * S);
+            const float h0 = fmaf(t.du, p0.y, p0.x);  // Alg. alg:subpixel lines 4-5
+            const float h1 = fmaf(t.du, p1.y, p1.x);
+            const float h2 = fmaf(t.du, p2.y, p2.x);
+            const float d01 = h1 - h0;
+            if (FULL || (kk >= kv0 && kk < kv1))
+                acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);  // line 6; Alg. alg:bp line 10
+            float fr1 = fr0 + t.dv;
+            const bool c = fr1 >= 1.f;
+            fr1 = c ? fr1 - 1.f : fr1;
+            const float lo = c ? h1 : h0;
+            const float d = c ? h2 - h1 : d01;
+            if (FULL || (kk + 1 >= kv0 && kk + 1 < kv1))
+                acc[kk + 1] = fmaf(t.W, fmaf(fr1, d, lo), acc[kk + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+            if ((kk & 7) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            if (!FULL && (kk < kv0 || kk >= kv1)) continue;
+            float fr;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
+            const uint32_t addr = bits * S + a0;
+            const float2 p0 = lds64(addr);
+            const float2 p1 = lds64(addr + S);
+            const float h0 = fmaf(t.du, p0.y, p0.x);
+            const float h1 = fmaf(t.du, p1.y, p1.x);
+            acc[kk] = fmaf(t.W, fmaf(fr, h1 - h0, h0), acc[kk]);
+        }
     }
 }
 
@@ -198,28 +231,52 @@ __device__ __forceinline__ float tapg(const float* __restrict__ Qv, int Nu, int 
     return __ldg(Qv + (long)r * Nu + col);
 }
 
-// One view from global memory (same arithmetic as the shared-memory path).
-template <int KC>
+// Horizontal lerp of detector row `row` from global memory, as the pair patch would give it.
+__device__ __forceinline__ float rowg(const float* Qv, const BPParams& p, const ThreadInv& t,
+                                      int row)
+{
+    const float a = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row, t.nu);
+    const float b = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row, t.nu + 1);
+    return fmaf(t.du, b - a, a);
+}
+
+// One view from global memory (bitwise the same arithmetic as the shared-memory path).
+template <int KC, bool PAIR>
 __device__ __forceinline__ void accumulate_view_global(float (&acc)[KC], const float* Qv,
                                                        const BPParams& p, const ThreadInv& t,
                                                        int kv0, int kv1)
 {
     float fv0 = t.fv0;
+    if constexpr (PAIR) {
 #pragma unroll
-    for (int kk = 0; kk < KC; ++kk) {
-        if ((kk & 3) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
-        if (kk < kv0 || kk >= kv1) continue;
-        float fr;
-        const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
-        const int row = t.nv + (int)(bits - 0x4B000000u);
-        const float a0 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row, t.nu);
-        const float b0 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row, t.nu + 1);
-        const float a1 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row + 1, t.nu);
-        const float b1 = tapg(Qv, p.Nu, p.Nv, p.v0, p.n_rows, row + 1, t.nu + 1);
-        const float h0 = fmaf(t.du, b0 - a0, a0);
-        const float h1 = fmaf(t.du, b1 - a1, a1);
-        const float val = fmaf(fr, h1 - h0, h0);
-        acc[kk] = fmaf(t.W, val, acc[kk]);
+        for (int kk = 0; kk < KC; kk += 2) {
+            if ((kk & 3) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            float fr0;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
+            const int row = t.nv + (int)(bits - 0x4B000000u);
+            const float h0 = rowg(Qv, p, t, row), h1 = rowg(Qv, p, t, row + 1),
+                        h2 = rowg(Qv, p, t, row + 2);
+            const float d01 = h1 - h0;
+            if (kk >= kv0 && kk < kv1) acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);
+            float fr1 = fr0 + t.dv;
+            const bool c = fr1 >= 1.f;
+            fr1 = c ? fr1 - 1.f : fr1;
+            const float lo = c ? h1 : h0;
+            const float d = c ? h2 - h1 : d01;
+            if (kk + 1 >= kv0 && kk + 1 < kv1)
+                acc[kk + 1] = fmaf(t.W, fmaf(fr1, d, lo), acc[kk + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+            if ((kk & 3) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            if (kk < kv0 || kk >= kv1) continue;
+            float fr;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
+            const int row = t.nv + (int)(bits - 0x4B000000u);
+            const float h0 = rowg(Qv, p, t, row), h1 = rowg(Qv, p, t, row + 1);
+            acc[kk] = fmaf(t.W, fmaf(fr, h1 - h0, h0), acc[kk]);
+        }
     }
 }
 
@@ -260,7 +317,10 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, in
     const double cj = (corner & 2) ? j_hi : j_lo;
     const ColInv c = column_invariants(P, ci, cj, (double)kb);
     double umin = c.u, umax = c.u;
-    const double va = c.v + kv0 * c.dv, vb = c.v + (kv1 - 1) * c.dv;
+    // slices whose rows are read: the PAIR walk reads from the even slice below kv0 to the odd
+    // slice at or above kv1 - 1, and one row more (h_need below)
+    const int ka = p.pair ? (kv0 & ~1) : kv0, kz = p.pair ? ((kv1 - 1) | 1) : kv1 - 1;
+    const double va = c.v + ka * c.dv, vb = c.v + kz * c.dv;
     double vmin = fmin(va, vb), vmax = fmax(va, vb);
 #pragma unroll
     for (int o = 1; o < 4; o <<= 1) {
@@ -276,7 +336,7 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, in
         // rounded down to a multiple of 4 floats.
         const bool finite = fu0 > -1e9 && fu1 < 1e9 && fv0 > -1e9 && fv1 < 1e9;
         const int u_org = finite ? (((int)fu0 - 1) & ~3) : 0;
-        const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0;
+        const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0 + p.pair;
         const bool fits = finite && w_need <= p.box_w && h_need <= p.box_h;
         m->u_org = u_org;
         m->v_org = finite ? (int)fv0 - 1 : 0;
@@ -286,7 +346,7 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, in
     }
 }
 
-template <int KC, int P2, bool TMA>
+template <int KC, int P2, bool TMA, bool PAIR>
 __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -394,11 +454,14 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
         if constexpr (TMA) {
             const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
             if (full)
-                accumulate_view_smem<KC, P2, true>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
+                accumulate_view_smem<KC, P2, true, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
+                                                         kv0, kv1);
             else
-                accumulate_view_smem<KC, P2, false>(acc, pb, p.neg_magic, ti, u_org, v_org, kv0, kv1);
+                accumulate_view_smem<KC, P2, false, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
+                                                          kv0, kv1);
         } else {
-            accumulate_view_global<KC>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0, kv1);
+            accumulate_view_global<KC, PAIR>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0,
+                                             kv1);
         }
         if (t == next_flush || t == n - 1) {
             if (active) flush<KC>(acc, p, i, j, kb, kv0, kv1, overwrite);
@@ -432,18 +495,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
-template <int KC, int P2>
+template <int KC, int P2, bool PAIR>
 ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, bool tma, dim3 grid, size_t smem,
                      cudaStream_t st)
 {
     cudaError_t e;
     if (tma) {
-        auto k = bp_kernel<KC, P2, true>;
+        auto k = bp_kernel<KC, P2, true, PAIR>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp)");
         k<<<grid, kThreads, smem, st>>>(p, map);
     } else {
-        auto k = bp_kernel<KC, P2, false>;
+        auto k = bp_kernel<KC, P2, false, PAIR>;
         k<<<grid, kThreads, 0, st>>>(p, map);
     }
     e = cudaGetLastError();
@@ -458,7 +521,7 @@ int choose_kc(const ifdk_geometry* g)
 {
     if (const char* e = std::getenv("IFDK_BP_KC")) {
         const int v = std::atoi(e);
-        if (v == 32 || v == 64) return v;
+        if (v == 32) return v;
     }
     (void)g;
     return 32;  // measured on B200, config 3/4: 32 slices (3 CTAs/SM) beat 64 (2 CTAs/SM) by 10%
@@ -515,7 +578,11 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     double wb, hb;
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
-    int box_h = (int)std::ceil(hb) + 6;
+    // PAIR walk: two slices per floor; valid while dv/dk = (D/Dv) Dz / z < 1 for every z.
+    const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
+    const char* pe = std::getenv("IFDK_BP_PAIR");
+    p.pair = (dv_max < 0.999 && !(pe && pe[0] == '0')) ? 1 : 0;
+    int box_h = (int)std::ceil(hb) + 6 + p.pair;
     if (box_w < 8) box_w = 8;
     int P2 = 0;
     for (int c : {24, 40, 56, 72})
@@ -548,19 +615,19 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
     dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
     ifdk_status s;
-    if (KC == 32) {
+    if (p.pair) {
         switch (P2) {
-            case 24: s = launch_t<32, 24>(p, map, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40>(p, map, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56>(p, map, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72>(p, map, tma, grid, smem, st); break;
+            case 24: s = launch_t<32, 24, true>(p, map, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40, true>(p, map, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56, true>(p, map, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72, true>(p, map, tma, grid, smem, st); break;
         }
     } else {
         switch (P2) {
-            case 24: s = launch_t<64, 24>(p, map, tma, grid, smem, st); break;
-            case 40: s = launch_t<64, 40>(p, map, tma, grid, smem, st); break;
-            case 56: s = launch_t<64, 56>(p, map, tma, grid, smem, st); break;
-            default: s = launch_t<64, 72>(p, map, tma, grid, smem, st); break;
+            case 24: s = launch_t<32, 24, false>(p, map, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40, false>(p, map, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56, false>(p, map, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72, false>(p, map, tma, grid, smem, st); break;
         }
     }
     cudaFreeAsync(Pd, st);
