@@ -394,14 +394,29 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
         const float* r = reinterpret_cast<const float*>(smem + (t & 1) * p.raw_bytes);
         float2* q = pair0 + (t & 1) * p.box_h * P2;
         const int wp = m.w_need - 1, hn = m.h_need;
-        for (int rr = warp; rr < hn; rr += kThreads / 32) {  // one detector row per warp
-            const float* rrow = r + rr * p.box_w;
-            for (int c0 = 0; c0 < wp; c0 += 32) {
-                const int cc = c0 + lane;
-                const float a = cc < p.box_w ? rrow[cc] : 0.f;
-                float b = __shfl_down_sync(0xffffffffu, a, 1);
-                if (lane == 31 && cc + 1 < p.box_w) b = rrow[cc + 1];
-                if (cc < wp) q[rr * P2 + cc] = make_float2(a, b - a);
+        if (p.box_w <= 32) {
+            // One detector row per warp and iteration, one column per lane; b = a of lane+1.
+            const float* rp = r + warp * p.box_w + lane;
+            float2* qp = q + warp * P2 + lane;
+            const bool in_box = lane < p.box_w, wr = lane < wp;
+            const int rstep = (kThreads / 32) * p.box_w;
+            for (int rr = warp; rr < hn; rr += kThreads / 32) {
+                const float a = in_box ? *rp : 0.f;
+                const float b = __shfl_down_sync(0xffffffffu, a, 1);
+                if (wr) *qp = make_float2(a, b - a);
+                rp += rstep;
+                qp += (kThreads / 32) * P2;
+            }
+        } else {
+            for (int rr = warp; rr < hn; rr += kThreads / 32) {
+                const float* rrow = r + rr * p.box_w;
+                for (int c0 = 0; c0 < wp; c0 += 32) {
+                    const int cc = c0 + lane;
+                    const float a = cc < p.box_w ? rrow[cc] : 0.f;
+                    float b = __shfl_down_sync(0xffffffffu, a, 1);
+                    if (lane == 31 && cc + 1 < p.box_w) b = rrow[cc + 1];
+                    if (cc < wp) q[rr * P2 + cc] = make_float2(a, b - a);
+                }
             }
         }
     };
