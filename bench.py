@@ -324,7 +324,7 @@ def run_ours(args, spec, rank, world, local_rank):
         import oracle
 
         oracle.build()
-        v, s, desc = oracle_sample(spec, 16, 1 << 24)  # ~10-20 s on the box's 16 cores
+        v, s, desc = oracle_sample(spec, 32, 1 << 25)  # ~10-20 s on the box's 16 cores
         cpu = {"value": v, "unit": "GUPS", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": desc, "seconds": s}
     value = gups(spec, ms / 1e3)

@@ -23,5 +23,6 @@ def metrics(got, ref):
 
 def assert_parity(got, ref, rmse_tol, max_tol, what=""):
     r, m = metrics(got, ref)
+    print(f"PARITY {what}: relRMSE {r:.3e}  max|d|/max|ref| {m:.3e}  (n={np.size(ref)})")
     assert r <= rmse_tol and m <= max_tol, f"{what}: relRMSE {r:.3e} (tol {rmse_tol}), max|d|/max|ref| {m:.3e} (tol {max_tol})"
     return r, m
