@@ -208,6 +208,8 @@ extern "C" void ifdk_geometry_destroy(ifdk_geometry* g)
     for (auto& d : g->dev) {
         if (d.Hs) cudaFree(d.Hs);
         if (d.tw) cudaFree(d.tw);
+        if (d.twA) cudaFree(d.twA);
+        if (d.twB) cudaFree(d.twB);
     }
     delete g;
 }

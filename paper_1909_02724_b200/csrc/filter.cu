@@ -13,6 +13,7 @@
 // passes), ping-ponging between two L-element complex buffers.  The roofline is HBM:
 // 8 algorithmic bytes per detector pixel (read E, write Q).
 #include <cmath>
+#include <vector>
 
 #include "ifdk_internal.h"
 
@@ -152,6 +153,178 @@ __global__ void __launch_bounds__(kThreads) filter_fft_kernel(const FilterParams
     }
 }
 
+
+// ----------------------------------------------------------------------------------------
+// Length-4096 FFT filter (Nu <= 2048): 256 threads, 16 complex values per thread, three
+// radix-16 Stockham passes (span 1, 16, 256) with the 16-point DFT in registers (4 x 4) and
+// two shared-memory exchanges per transform.  Pass 1 reads the rows straight from HBM (the
+// upper half of the padded signal is zero), the last forward pass leaves thread i holding
+// X[i + 256 m], which is exactly the input the inverse's first pass needs, so the filter
+// multiply and the conj of the inverse happen in registers; the inverse's last pass leaves
+// Z[i + 256 m] and the first Nu samples go straight back to HBM.
+namespace f4k {
+
+constexpr int L = 4096, T = 256;
+
+__device__ __forceinline__ int padx(int q) { return q + (q >> 4); }  // 1 pad word per 16
+
+__device__ __forceinline__ float2 cmulf(float2 a, float2 b)
+{
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+
+__device__ __forceinline__ void dft4(float2& a, float2& b, float2& c, float2& d)
+{
+    const float2 t0 = make_float2(a.x + c.x, a.y + c.y), t1 = make_float2(a.x - c.x, a.y - c.y);
+    const float2 t2 = make_float2(b.x + d.x, b.y + d.y);
+    const float2 t3 = make_float2(b.y - d.y, d.x - b.x);  // -i (b - d)
+    a = make_float2(t0.x + t2.x, t0.y + t2.y);
+    c = make_float2(t0.x - t2.x, t0.y - t2.y);
+    b = make_float2(t1.x + t3.x, t1.y + t3.y);
+    d = make_float2(t1.x - t3.x, t1.y - t3.y);
+}
+
+// 16-point forward DFT in place: n = 4 n1 + n2, k = k1 + 4 k2 (two radix-4 stages).
+__device__ __forceinline__ void dft16(float2 (&u)[16])
+{
+    constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f,
+                    C2 = 0.70710678118654752f;
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) dft4(u[n2], u[4 + n2], u[8 + n2], u[12 + n2]);
+    // A[n2][k1] (at u[4 k1 + n2]) *= W16^(n2 k1)
+    u[5] = cmulf(u[5], make_float2(C1, -S1));    // W^1
+    u[6] = cmulf(u[6], make_float2(C2, -C2));    // W^2
+    u[7] = cmulf(u[7], make_float2(S1, -C1));    // W^3
+    u[9] = cmulf(u[9], make_float2(C2, -C2));    // W^2
+    u[10] = make_float2(u[10].y, -u[10].x);      // W^4 = -i
+    u[11] = cmulf(u[11], make_float2(-C2, -C2)); // W^6
+    u[13] = cmulf(u[13], make_float2(S1, -C1));  // W^3
+    u[14] = cmulf(u[14], make_float2(-C2, -C2)); // W^6
+    u[15] = cmulf(u[15], make_float2(-C1, S1));  // W^9
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft4(u[4 * k1], u[4 * k1 + 1], u[4 * k1 + 2], u[4 * k1 + 3]);
+    // X[k1 + 4 k2] sits at u[4 k1 + k2]: transpose by renaming
+    float2 v[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = u[4 * (m & 3) + (m >> 2)];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) u[m] = v[m];
+}
+
+// Twiddle w^e, w = exp(-2 pi i / 4096), from two small tables: w^(16 a) and w^b.
+__device__ __forceinline__ float2 twiddle(const float2* twA, const float2* twB, int e)
+{
+    const float2 a = twA[e >> 4];
+    const int b = e & 15;
+    return b ? cmulf(a, twB[b]) : a;
+}
+
+// One Stockham radix-16 pass of span P on the values u (= x[i + 256 j]) of thread i; writes
+// the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
+template <int P>
+__device__ __forceinline__ void pass_out(float2 (&u)[16], float2* buf, const float2* twA,
+                                         const float2* twB, int i)
+{
+    const int k = i & (P - 1);
+    if (P > 1) {
+#pragma unroll
+        for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], twiddle(twA, twB, j * k * (256 / P)));
+    }
+    dft16(u);
+    const int base = (i - k) * 16 + k;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) buf[padx(base + m * P)] = u[m];
+}
+
+__device__ __forceinline__ void load_in(float2 (&u)[16], const float2* buf, int i)
+{
+#pragma unroll
+    for (int j = 0; j < 16; ++j) u[j] = buf[padx(i + j * T)];
+}
+
+// Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
+// X[i + 256 m].  Uses buf for the two exchanges.
+__device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf, const float2* twA,
+                                        const float2* twB, int i)
+{
+    pass_out<1>(u, buf, twA, twB, i);
+    __syncthreads();
+    load_in(u, buf, i);
+    __syncthreads();
+    pass_out<16>(u, buf, twA, twB, i);
+    __syncthreads();
+    load_in(u, buf, i);
+    __syncthreads();
+    const int k = i;  // span 256: k = i, outputs at i + 256 m stay in this thread
+#pragma unroll
+    for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], twiddle(twA, twB, j * k));
+    dft16(u);
+}
+
+}  // namespace f4k
+
+__global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p,
+                                                            const float2* __restrict__ twA_g,
+                                                            const float2* __restrict__ twB_g,
+                                                            const float* __restrict__ Hs_g)
+{
+    using namespace f4k;
+    __shared__ float2 buf[L + L / 16];
+    __shared__ float2 twA[256];
+    __shared__ float2 twB[16];
+    __shared__ float Hs[L / 2 + 1];
+    const int i = threadIdx.x;
+    twA[i] = twA_g[i];
+    if (i < 16) twB[i] = twB_g[i];
+    for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
+    __syncthreads();
+    const long n_pairs = (p.n_rows_total + 1) / 2;
+    for (long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
+        const long rA = 2 * pr, rB = 2 * pr + 1;
+        const bool hasB = rB < p.n_rows_total;
+        const float vhA = ((float)(p.v0 + (int)(rA % p.n_rows)) - p.cv) * p.Dv;
+        const float vhB = ((float)(p.v0 + (int)(rB % p.n_rows)) - p.cv) * p.Dv;
+        const float dA = p.D2 + vhA * vhA, dB = p.D2 + vhB * vhB;
+        const float* eA = p.raw + rA * p.Nu;
+        const float* eB = p.raw + rB * p.Nu;
+        float2 u[16];
+        // Alg. alg:filter line 2: E~ = E . F_cos (reading c-A5), rows A | B packed, zero padded.
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int n = i + j * T;
+            float2 x = make_float2(0.f, 0.f);
+            if (j < 8 && n < p.Nu) {
+                const float uh = ((float)n - p.cu) * p.Du;
+                x.x = __ldg(eA + n) * (p.D / sqrtf(dA + uh * uh));
+                if (hasB) x.y = __ldg(eB + n) * (p.D / sqrtf(dB + uh * uh));
+            }
+            u[j] = x;
+        }
+        __syncthreads();  // buf is free (previous pair fully read)
+        fft4096(u, buf, twA, twB, i);
+        // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int f = i + m * T;
+            const float h = Hs[f <= L / 2 ? f : L - f];
+            u[m] = make_float2(u[m].x * h, -u[m].y * h);
+        }
+        __syncthreads();
+        fft4096(u, buf, twA, twB, i);
+        // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1.
+        float* qA = p.out + rA * p.Nu;
+        float* qB = p.out + rB * p.Nu;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int n = i + m * T;
+            if (n < p.Nu) {
+                qA[n] = u[m].x;
+                if (hasB) qB[n] = -u[m].y;
+            }
+        }
+    }
+}
+
 }  // namespace
 
 ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
@@ -174,23 +347,30 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
             cudaMemcpy(D.Hs, g->Hs.data(), sizeof(float) * (L / 2 + 1), cudaMemcpyHostToDevice);
             e = cudaMemcpy(D.tw, g->tw.data(), sizeof(float2) * L, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(filter tables)");
+            if (L == 4096) {
+                std::vector<float> a(512), b(32);
+                for (int q = 0; q < 256; ++q) {
+                    a[2 * q] = g->tw[2 * (16 * q)];
+                    a[2 * q + 1] = g->tw[2 * (16 * q) + 1];
+                }
+                for (int q = 0; q < 16; ++q) {
+                    b[2 * q] = g->tw[2 * q];
+                    b[2 * q + 1] = g->tw[2 * q + 1];
+                }
+                if ((e = cudaMalloc(&D.twA, sizeof(float2) * 256)) != cudaSuccess ||
+                    (e = cudaMalloc(&D.twB, sizeof(float2) * 16)) != cudaSuccess)
+                    return cuda_fail(e, "cudaMalloc(twiddles)");
+                cudaMemcpy(D.twA, a.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
+                e = cudaMemcpy(D.twB, b.data(), sizeof(float2) * 16, cudaMemcpyHostToDevice);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(filter tables)");
+            }
         }
     }
     const long total = n_views * (long)n_rows;
     if (total == 0) return IFDK_OK;
     const int L = 1 << g->log2L;
-    const size_t smem = 2 * sizeof(float2) * (size_t)L;
-    e = cudaFuncSetAttribute(filter_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, filter_fft_kernel, kThreads, smem);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (per_sm < 1) return fail(IFDK_ERR_SHAPE, "Nu too large for the shared-memory FFT");
-    const long pairs = (total + 1) / 2;
-    long grid = (long)sms * per_sm;
-    if (grid > pairs) grid = pairs;
     FilterParams p;
     p.raw = raw;
     p.out = out;
@@ -204,6 +384,26 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
     p.Dv = (float)g->Dv;
     p.cu = (float)g->cu;
     p.cv = (float)g->cv;
+    const long pairs = (total + 1) / 2;
+    if (L == 4096) {
+        long grid = (long)sms * 2;
+        if (grid > pairs) grid = pairs;
+        filter_f4k_kernel<<<(unsigned)grid, 256, 0, st>>>(p, g->dev[dev].twA, g->dev[dev].twB,
+                                                          g->dev[dev].Hs);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "filter_f4k_kernel launch");
+        count_launch();
+        return IFDK_OK;
+    }
+    const size_t smem = 2 * sizeof(float2) * (size_t)L;
+    e = cudaFuncSetAttribute(filter_fft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, filter_fft_kernel, kThreads, smem);
+    if (per_sm < 1) return fail(IFDK_ERR_SHAPE, "Nu too large for the shared-memory FFT");
+    long grid = (long)sms * per_sm;
+    if (grid > pairs) grid = pairs;
     filter_fft_kernel<<<(unsigned)grid, kThreads, smem, st>>>(p, g->dev[dev].tw, g->dev[dev].Hs,
                                                               g->log2L);
     e = cudaGetLastError();

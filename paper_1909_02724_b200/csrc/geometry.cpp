@@ -89,9 +89,11 @@ void patch_bound(const ifdk_geometry* g, int ti, int tj, int kc, double* w, doub
 void ensure_filter_tables_host(ifdk_geometry* g)
 {
     if (g->log2L) return;
-    int log2L = 1;
-    while ((1 << log2L) < 2 * g->Nu - 1) ++log2L;
-    if (log2L < 2) log2L = 2;
+    // Nu <= 2048: the register radix-16 kernel of fixed length 4096 (any L >= 2 Nu - 1 gives
+    // the same linear convolution); larger rows: the generic Stockham kernel, minimal L.
+    int log2L = 12;
+    if (g->Nu > 2048)
+        while ((1 << log2L) < 2 * g->Nu - 1) ++log2L;
     const int L = 1 << log2L;
     const double pi = 3.14159265358979323846;
     std::vector<double> h(g->Nu, 0.0);

@@ -25,6 +25,8 @@ struct ifdk_geometry {
     struct Dev {
         float* Hs = nullptr;
         float2* tw = nullptr;
+        float2* twA = nullptr;  // w^(16 a), a < 256 (length-4096 kernel)
+        float2* twB = nullptr;  // w^b, b < 16
     } dev[32];
     std::mutex mu;
 };

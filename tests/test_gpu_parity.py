@@ -47,6 +47,7 @@ def _oracle_Q32(spec, E, v0=0):
     (37, 5, 1, 0),       # odd Nu, a single view
     (512, 8, 4, 200),    # a row band in the middle of the detector
     (2048, 3, 2, 1000),  # L = 4096, the config-4/5 row length
+    (2100, 2, 3, 0),     # Nu > 2048: the generic Stockham kernel (L = 8192)
 ])
 def test_filter_matches_oracle(torch_cuda, Nu, n_rows, n_views, v0):
     torch = torch_cuda
