@@ -530,16 +530,26 @@ ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, bool tma, dim3 g
     return IFDK_OK;
 }
 
+// PAIR walk: two slices per floor; valid while dv/dk = (D/Dv) Dz / z < 1 for every z.
+bool use_pair(const ifdk_geometry* g)
+{
+    const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
+    const char* pe = std::getenv("IFDK_BP_PAIR");
+    return dv_max < 0.999 && !(pe && pe[0] == '0');
+}
+
 // Slices per k-chunk (= register accumulators per thread).  The choice depends on the geometry
 // only, never on the slab, so every decomposition of a volume walks identical chunks.
+// Measured on B200 (config 4): PAIR with 64 slices (2 CTAs/SM, 128 registers) 1724 GUPS vs
+// 32 slices (3 CTAs/SM, 80 registers) 1586; without PAIR 32 slices win.
 int choose_kc(const ifdk_geometry* g)
 {
+    const bool pair = use_pair(g);
     if (const char* e = std::getenv("IFDK_BP_KC")) {
         const int v = std::atoi(e);
-        if (v == 32) return v;
+        if (v == 32 || (v == 64 && pair)) return v;
     }
-    (void)g;
-    return 32;  // measured on B200, config 3/4: 32 slices (3 CTAs/SM) beat 64 (2 CTAs/SM) by 10%
+    return pair ? 64 : 32;
 }
 
 }  // namespace
@@ -593,10 +603,7 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     double wb, hb;
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
-    // PAIR walk: two slices per floor; valid while dv/dk = (D/Dv) Dz / z < 1 for every z.
-    const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
-    const char* pe = std::getenv("IFDK_BP_PAIR");
-    p.pair = (dv_max < 0.999 && !(pe && pe[0] == '0')) ? 1 : 0;
+    p.pair = use_pair(g) ? 1 : 0;
     int box_h = (int)std::ceil(hb) + 6 + p.pair;
     if (box_w < 8) box_w = 8;
     int P2 = 0;
@@ -630,7 +637,14 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
     dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
     ifdk_status s;
-    if (p.pair) {
+    if (p.pair && KC == 64) {
+        switch (P2) {
+            case 24: s = launch_t<64, 24, true>(p, map, tma, grid, smem, st); break;
+            case 40: s = launch_t<64, 40, true>(p, map, tma, grid, smem, st); break;
+            case 56: s = launch_t<64, 56, true>(p, map, tma, grid, smem, st); break;
+            default: s = launch_t<64, 72, true>(p, map, tma, grid, smem, st); break;
+        }
+    } else if (p.pair) {
         switch (P2) {
             case 24: s = launch_t<32, 24, true>(p, map, tma, grid, smem, st); break;
             case 40: s = launch_t<32, 40, true>(p, map, tma, grid, smem, st); break;

@@ -24,7 +24,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Callable, Optional
 
-KC = 64          # k-chunk of the BP kernel (backproject.cu kKC)
+KC = 64          # slab starts are multiples of the BP kernel k-chunk (32 or 64, backproject.cu)
 VIEW_BATCH = 128  # two-level summation batch of the BP kernel (BPParams.vb)
 
 

@@ -76,7 +76,8 @@ def test_full_config_sampled_parity(torch_cuda, cfg):
     cz = spec.Nz // 2
     samples = {
         "central": _sample(spec, [(cz - 24, cz + 24)], [1 << 14], rng),
-        "bottom": _sample(spec, [(0, 12)], [1 << 13], rng),
+        # low slices that still cut the phantom (its z half-extent is 0.9 x 0.9 x 90 mm)
+        "low": _sample(spec, [(spec.Nz // 10, spec.Nz // 10 + 12)], [1 << 13], rng),
     }
     for name, ijk in samples.items():
         lo, hi = _band(g, spec, ijk)
@@ -84,6 +85,7 @@ def test_full_config_sampled_parity(torch_cuda, cfg):
         ref = _oracle_on_sample(spec, E_band, lo, ijk)
         idx = torch.from_numpy(ijk.astype(np.int64)).cuda()
         got = vol[idx[:, 2], idx[:, 1], idx[:, 0]].cpu().numpy()
+        assert np.abs(ref).max() > 0.05, f"{name} sample misses the phantom"
         assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL, f"config {cfg} {name} sample")
 
 
@@ -102,7 +104,7 @@ def test_config5_slab0_sampled_parity(torch_cuda):
     batch = 256
     Q = torch.empty((batch, spec.Nv, spec.Nu), device="cuda")
     rng = np.random.default_rng(SEED)
-    ijk = _sample(spec, [(k0, k0 + 8)], [1 << 13], rng)
+    ijk = _sample(spec, [(k0 + nk - 16, k0 + nk - 8)], [1 << 13], rng)  # cuts the phantom
     lo_s, hi_s = _band(g, spec, ijk)
     E_band = np.empty((spec.Np, hi_s - lo_s + 1, spec.Nu), np.float32)
     for b0 in range(0, spec.Np, batch):
@@ -117,4 +119,5 @@ def test_config5_slab0_sampled_parity(torch_cuda):
     ref = _oracle_on_sample(spec, E_band, lo_s, ijk)
     idx = torch.from_numpy(ijk.astype(np.int64)).cuda()
     got = vol[idx[:, 2] - k0, idx[:, 1], idx[:, 0]].cpu().numpy()
+    assert np.abs(ref).max() > 0.05, "sample misses the phantom"
     assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL, "config 5 slab 0 sample")
