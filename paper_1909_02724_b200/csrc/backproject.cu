@@ -134,7 +134,7 @@ __device__ __forceinline__ ColInv column_invariants(const double* P, double i, d
 // Thread-side split of the invariants: integer detector column/row + fp32 fractions.
 struct ThreadInv {
     int nu, nv;
-    float du, fv0, dv, W;
+    float du, fv0, dv, dvm1, W;
 };
 
 __device__ __forceinline__ ThreadInv split(const ColInv& c)
@@ -146,6 +146,7 @@ __device__ __forceinline__ ThreadInv split(const ColInv& c)
     t.du = (float)(c.u - fu);
     t.fv0 = (float)(c.v - fv);
     t.dv = (float)c.dv;
+    t.dvm1 = t.dv - 1.f;
     t.W = (float)(c.f * c.f);  // W_dis = f^2, Alg. alg:bp line 8
     return t;
 }
@@ -164,7 +165,7 @@ __device__ __forceinline__ uint32_t floor_bits(float v, float* fr)
 // PAIR (needs dv < 1 px per slice, true for every config): two consecutive slices kk, kk+1
 // touch at most three detector rows n, n+1, n+2 (v grows by dv < 1), so one floor, three
 // LDS.64 and three horizontal lerps serve both updates: slice kk+1 uses rows (n, n+1) or
-// (n+1, n+2) depending on whether fr + dv crosses 1.  12 B of shared memory per update
+// (n+1, n+2) depending on whether fr + dv crosses 1 (one FSEL, no second floor).  12 B of shared memory per update
 // instead of 16.  The partial-chunk path runs the same arithmetic and only masks the
 // accumulation, so a slab split never changes a bit.
 template <int KC, int P2, bool FULL, bool PAIR>
@@ -197,13 +198,12 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
             const float d01 = h1 - h0;
             if (FULL || (kk >= kv0 && kk < kv1))
                 acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);  // line 6; Alg. alg:bp line 10
-            float fr1 = fr0 + t.dv;
-            const bool c = fr1 >= 1.f;
-            fr1 = c ? fr1 - 1.f : fr1;
-            const float lo = c ? h1 : h0;
-            const float d = c ? h2 - h1 : d01;
+            // slice kk+1 sits g = fr0 + dv - 1 rows past row n+1 (g in [-1, 1)): interpolate
+            // from h1 towards h2 (g >= 0) or back towards h0 (g < 0, h1 + g d01 = h0 + (1+g) d01).
+            const float g = fr0 + t.dvm1;
+            const float d = g >= 0.f ? h2 - h1 : d01;
             if (FULL || (kk + 1 >= kv0 && kk + 1 < kv1))
-                acc[kk + 1] = fmaf(t.W, fmaf(fr1, d, lo), acc[kk + 1]);
+                acc[kk + 1] = fmaf(t.W, fmaf(g, d, h1), acc[kk + 1]);
         }
     } else {
 #pragma unroll
@@ -258,13 +258,9 @@ __device__ __forceinline__ void accumulate_view_global(float (&acc)[KC], const f
                         h2 = rowg(Qv, p, t, row + 2);
             const float d01 = h1 - h0;
             if (kk >= kv0 && kk < kv1) acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);
-            float fr1 = fr0 + t.dv;
-            const bool c = fr1 >= 1.f;
-            fr1 = c ? fr1 - 1.f : fr1;
-            const float lo = c ? h1 : h0;
-            const float d = c ? h2 - h1 : d01;
-            if (kk + 1 >= kv0 && kk + 1 < kv1)
-                acc[kk + 1] = fmaf(t.W, fmaf(fr1, d, lo), acc[kk + 1]);
+            const float g = fr0 + t.dvm1;
+            const float d = g >= 0.f ? h2 - h1 : d01;
+            if (kk + 1 >= kv0 && kk + 1 < kv1) acc[kk + 1] = fmaf(t.W, fmaf(g, d, h1), acc[kk + 1]);
         }
     } else {
 #pragma unroll
