@@ -168,10 +168,14 @@ __device__ __forceinline__ uint32_t floor_bits(float v, float* fr)
 // (n+1, n+2) depending on whether fr + dv crosses 1 (one FSEL, no second floor).  12 B of shared memory per update
 // instead of 16.  The partial-chunk path runs the same arithmetic and only masks the
 // accumulation, so a slab split never changes a bit.
-template <int KC, int P2, bool FULL, bool PAIR>
+// `hook(q)` runs once per 8-slice group q (0 .. KC/8 - 1) in program order with the group's
+// updates: the kernel uses it to transform row q of the next view's patch while this view's
+// shared loads are in flight.
+template <int KC, int P2, bool FULL, bool PAIR, typename Hook>
 __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t pair_base,
                                                      uint32_t neg_magic, const ThreadInv& t,
-                                                     int u_org, int v_org, int kv0, int kv1)
+                                                     int u_org, int v_org, int kv0, int kv1,
+                                                     Hook&& hook)
 {
     // byte address of pair (row nv + n, col nu) = pair_base + ((nv - v_org + n) P2 + nu - u_org) 8
     // neg_magic = -0x4B000000 * P2 * 8 (mod 2^32) arrives as a kernel parameter so that ptxas
@@ -185,7 +189,10 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
         for (int kk = 0; kk < KC; kk += 2) {
             // Every 8 slices, launder fv0 through a volatile asm so that the compiler cannot
             // hoist the address arithmetic of later slices above earlier shared loads.
-            if ((kk & 7) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            if ((kk & 7) == 0) {
+                hook(kk >> 3);
+                asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            }
             float fr0;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
             const uint32_t addr = bits * S + a0;
@@ -208,7 +215,10 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
     } else {
 #pragma unroll
         for (int kk = 0; kk < KC; ++kk) {
-            if ((kk & 7) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            if ((kk & 7) == 0) {
+                hook(kk >> 3);
+                asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            }
             if (!FULL && (kk < kv0 || kk >= kv1)) continue;
             float fr;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
@@ -463,13 +473,46 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
         }
         const ThreadInv ti = split(column_invariants(Pr, di, dj, dkb));
         if constexpr (TMA) {
+            // Next view's raw box (TMA issued two iterations ago, normally landed): rewrite it
+            // into pairs row by row inside this view's update loop (one row per warp per
+            // 8-slice group), the rest after.
+            const bool nxt = t + 1 < n;
+            int hn = 0, wp = 0;
+            const float* rbase = nullptr;
+            float2* qbase = nullptr;
+            if (nxt) {
+                mbar_wait(&mbar[(t + 1) & 1], (uint32_t)(((t + 1) >> 1) & 1));
+                const Meta& mn = meta[(t + 1) & (kMetaRing - 1)];
+                if (!mn.fast) __trap();  // the host sizes the box from a conservative bound
+                hn = mn.h_need;
+                wp = mn.w_need - 1;
+                rbase = reinterpret_cast<const float*>(smem + ((t + 1) & 1) * p.raw_bytes);
+                qbase = pair0 + ((t + 1) & 1) * p.box_h * P2;
+            }
+            const bool narrow = p.box_w <= 32;
+            const bool in_box = lane < p.box_w, wr = lane < wp;
+            auto row = [&](int q) {  // transform row warp + 8 q of the next view (narrow boxes)
+                const int rr = warp + (kThreads / 32) * q;
+                if (narrow && rr < hn) {
+                    const float a = in_box ? rbase[rr * p.box_w + lane] : 0.f;
+                    const float b = __shfl_down_sync(0xffffffffu, a, 1);
+                    if (wr) qbase[rr * P2 + lane] = make_float2(a, b - a);
+                }
+            };
             const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
             if (full)
                 accumulate_view_smem<KC, P2, true, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
-                                                         kv0, kv1);
+                                                         kv0, kv1, row);
             else
                 accumulate_view_smem<KC, P2, false, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
-                                                          kv0, kv1);
+                                                          kv0, kv1, row);
+            if (nxt) {
+                if (narrow) {
+                    for (int q = KC / 8; warp + (kThreads / 32) * q < hn; ++q) row(q);
+                } else {
+                    transform(t + 1);
+                }
+            }
         } else {
             accumulate_view_global<KC, PAIR>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0,
                                              kv1);
@@ -480,11 +523,6 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
             next_flush += p.vb;
         }
         if (TMA) {
-            if (t + 1 < n) {
-                mbar_wait(&mbar[(t + 1) & 1], (uint32_t)(((t + 1) >> 1) & 1));
-                if (!meta[(t + 1) & (kMetaRing - 1)].fast) __trap();
-                transform(t + 1);
-            }
             if (((t + 3) & 7) == 0) metas(t + 3);
             __syncthreads();
             if (tid == 0 && t + 3 < n) issue(t + 3);
