@@ -146,6 +146,8 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
         cudaEventCreateWithFlags(&copied[q], cudaEventDisableTiming);
         cudaEventCreateWithFlags(&consumed[q], cudaEventDisableTiming);
     }
+    cudaEvent_t slab_done = nullptr;
+    cudaEventCreateWithFlags(&slab_done, cudaEventDisableTiming);
     e = cudaMallocAsync(&vol, sizeof(float) * vol_elems, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&buf[0], sizeof(float) * view_elems * batch, st);
     if (e == cudaSuccess) e = cudaMallocAsync(&buf[1], sizeof(float) * view_elems * batch, st);
@@ -177,15 +179,40 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
             cudaStreamWaitEvent(st, copied[q], 0);
             s = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb, 0, g->Nv, st);
             if (s != IFDK_OK) break;
-            s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vol, 0, g->Nz, b0 > 0 ? 1 : 0, st);
-            launches += 2;
+            ++launches;
+            if (b + 1 < nbatches) {
+                s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vol, 0, g->Nz,
+                                       b0 > 0 ? 1 : 0, st);
+                ++launches;
+            } else {
+                // Last batch: back-project slab by slab and stream each finished slab to the
+                // host on `cp` while the next slab computes (slab starts on multiples of 64
+                // slices, so the result is bitwise that of one launch).
+                const int slab = g->Nz > 512 ? 256 : g->Nz;
+                for (int k0 = 0; k0 < g->Nz && s == IFDK_OK; k0 += slab) {
+                    const int nk = (g->Nz - k0) < slab ? (g->Nz - k0) : slab;
+                    float* vs = vol + (size_t)k0 * g->Ny * g->Nx;
+                    s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vs, k0, nk,
+                                           b0 > 0 ? 1 : 0, st);
+                    ++launches;
+                    cudaEventRecord(slab_done, st);
+                    cudaStreamWaitEvent(cp, slab_done, 0);
+                    e = cudaMemcpyAsync(vol_host + (size_t)k0 * g->Ny * g->Nx, vs,
+                                        sizeof(float) * (size_t)nk * g->Ny * g->Nx,
+                                        cudaMemcpyDeviceToHost, cp);
+                    if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(volume D2H)");
+                }
+            }
             cudaEventRecord(consumed[q], st);
             if (b + 2 < nbatches) enqueue_copy(b + 2);
         }
-        if (s == IFDK_OK) {
+        if (s == IFDK_OK && nbatches == 0) {
             e = cudaMemcpyAsync(vol_host, vol, sizeof(float) * vol_elems, cudaMemcpyDeviceToHost, st);
             if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(volume D2H)");
         }
+        // the copy stream must finish before the scratch is released on `st`
+        cudaEventRecord(slab_done, cp);
+        cudaStreamWaitEvent(st, slab_done, 0);
     }
     if (buf[0]) cudaFreeAsync(buf[0], st);
     if (buf[1]) cudaFreeAsync(buf[1], st);
@@ -197,6 +224,7 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
         cudaEventDestroy(copied[q]);
         cudaEventDestroy(consumed[q]);
     }
+    cudaEventDestroy(slab_done);
     cudaStreamDestroy(cp);
     t_launches = launches;
     return s;

@@ -229,16 +229,19 @@ def test_reconstruct_noisy_stress_input(torch_cuda):
     assert_parity(vol.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "reconstruct noisy")
 
 
-def test_reconstruct_host_equals_device(torch_cuda):
+@pytest.mark.parametrize("shape", [(48, 48, 48), (600, 24, 40)])  # (Nz, Ny, Nx)
+def test_reconstruct_host_equals_device(torch_cuda, shape):
+    """> one 256-view batch; Nz = 600 streams the last batch's volume to the host in slabs."""
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_reconstruct, ifdk_reconstruct_host
 
-    spec = _spec(300, 64, 64, 48, 48, 48)  # > one 256-view batch
+    Nz, Ny, Nx = shape
+    spec = _spec(300, 64, 64, Nx, Ny, Nz)
     g = Geometry.from_spec(spec)
     E = _phantom_E(spec)
-    vol_d = torch.empty((48, 48, 48), device="cuda")
+    vol_d = torch.empty(shape, device="cuda")
     ifdk_reconstruct(g, torch.from_numpy(E).cuda(), vol_d)
-    vol_h = np.empty((48, 48, 48), np.float32)
+    vol_h = np.empty(shape, np.float32)
     ifdk_reconstruct_host(g, E, vol_h)
     assert np.array_equal(vol_h, vol_d.cpu().numpy())
 
