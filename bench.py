@@ -111,12 +111,14 @@ def measured_peaks():
 
 
 def ncu_traffic(config: int):
-    """DRAM bytes per BP launch from the committed ncu --set full capture, if present."""
+    """DRAM bytes (read + write) per bench BP launch from the committed ncu --set full capture
+    (profiles/ncu_bp_traffic.json: a 256-view x 256-slice launch scaled by updates), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_bp_traffic.json")
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return d.get(str(config))
+        e = d.get(str(config))
+        return e["bytes_per_launch"] if e else None
     return None
 
 

@@ -13,6 +13,7 @@
 // passes), ping-ponging between two L-element complex buffers.  The roofline is HBM:
 // 8 algorithmic bytes per detector pixel (read E, write Q).
 #include <cmath>
+#include <cstdint>
 #include <vector>
 
 #include "ifdk_internal.h"
@@ -263,30 +264,59 @@ __device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf, const floa
 
 }  // namespace f4k
 
+// ASYNC (rows 16-byte aligned, Nu % 4 == 0): the next row pair is fetched into a shared
+// staging buffer with cp.async while the current pair is transformed, hiding HBM latency.
+constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
+constexpr size_t kF4kSmem = sizeof(float2) * (4096 + 256) + sizeof(float2) * (256 + 16) +
+                            sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage;
+
+template <bool ASYNC>
 __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p,
                                                             const float2* __restrict__ twA_g,
                                                             const float2* __restrict__ twB_g,
                                                             const float* __restrict__ Hs_g)
 {
     using namespace f4k;
-    __shared__ float2 buf[L + L / 16];
-    __shared__ float2 twA[256];
-    __shared__ float2 twB[16];
-    __shared__ float Hs[L / 2 + 1];
+    extern __shared__ __align__(16) unsigned char fsm[];
+    float2* const buf = reinterpret_cast<float2*>(fsm);  // L + L/16 (padded)
+    float2* const twA = buf + (L + L / 16);                // 256
+    float2* const twB = twA + 256;                          // 16
+    float* const Hs = reinterpret_cast<float*>(twB + 16);   // L/2 + 1 (2052 slots)
+    float* const stage = Hs + 2052;                         // 2 rows
     const int i = threadIdx.x;
     twA[i] = twA_g[i];
     if (i < 16) twB[i] = twB_g[i];
     for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
-    __syncthreads();
     const long n_pairs = (p.n_rows_total + 1) / 2;
+    auto prefetch = [&](long pr) {
+        if (!ASYNC || pr >= n_pairs) return;
+        const long rA = 2 * pr;
+        const int nrow = (2 * pr + 1 < p.n_rows_total) ? 2 : 1;
+        const int q4 = p.Nu / 4;
+        for (int c = i; c < nrow * q4; c += T) {
+            const int r = c >= q4, cc = c - r * q4;
+            const float* src = p.raw + (rA + r) * p.Nu + 4 * cc;
+            const uint32_t dst =
+                static_cast<uint32_t>(__cvta_generic_to_shared(stage + r * kF4kStage + 4 * cc));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src)
+                         : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    prefetch(blockIdx.x);
+    __syncthreads();
     for (long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
         const long rA = 2 * pr, rB = 2 * pr + 1;
         const bool hasB = rB < p.n_rows_total;
         const float vhA = ((float)(p.v0 + (int)(rA % p.n_rows)) - p.cv) * p.Dv;
         const float vhB = ((float)(p.v0 + (int)(rB % p.n_rows)) - p.cv) * p.Dv;
         const float dA = p.D2 + vhA * vhA, dB = p.D2 + vhB * vhB;
-        const float* eA = p.raw + rA * p.Nu;
-        const float* eB = p.raw + rB * p.Nu;
+        const float* eA = ASYNC ? stage : p.raw + rA * p.Nu;
+        const float* eB = ASYNC ? stage + kF4kStage : p.raw + rB * p.Nu;
+        if (ASYNC) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        }
         float2 u[16];
         // Alg. alg:filter line 2: E~ = E . F_cos (reading c-A5), rows A | B packed, zero padded.
 #pragma unroll
@@ -295,12 +325,13 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             float2 x = make_float2(0.f, 0.f);
             if (j < 8 && n < p.Nu) {
                 const float uh = ((float)n - p.cu) * p.Du;
-                x.x = __ldg(eA + n) * (p.D / sqrtf(dA + uh * uh));
-                if (hasB) x.y = __ldg(eB + n) * (p.D / sqrtf(dB + uh * uh));
+                x.x = (ASYNC ? eA[n] : __ldg(eA + n)) * (p.D / sqrtf(dA + uh * uh));
+                if (hasB) x.y = (ASYNC ? eB[n] : __ldg(eB + n)) * (p.D / sqrtf(dB + uh * uh));
             }
             u[j] = x;
         }
-        __syncthreads();  // buf is free (previous pair fully read)
+        __syncthreads();  // staging read and buf free: fetch the next pair while this one runs
+        prefetch(pr + gridDim.x);
         fft4096(u, buf, twA, twB, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
 #pragma unroll
@@ -323,6 +354,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             }
         }
     }
+    if (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 }  // namespace
@@ -388,8 +420,14 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
     if (L == 4096) {
         long grid = (long)sms * 2;
         if (grid > pairs) grid = pairs;
-        filter_f4k_kernel<<<(unsigned)grid, 256, 0, st>>>(p, g->dev[dev].twA, g->dev[dev].twB,
-                                                          g->dev[dev].Hs);
+        // In-place filtering is safe with the prefetch: a pair's rows are fetched before any
+        // CTA writes them (each pair belongs to one CTA) and never read again.
+        const bool async = (g->Nu % 4) == 0 && (reinterpret_cast<uintptr_t>(raw) % 16) == 0;
+        auto k = async ? filter_f4k_kernel<true> : filter_f4k_kernel<false>;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4kSmem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
+        k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].twA, g->dev[dev].twB,
+                                                 g->dev[dev].Hs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "filter_f4k_kernel launch");
         count_launch();
