@@ -244,18 +244,17 @@ __device__ __forceinline__ void load_in(float2 (&u)[16], const float2* buf, int 
 }
 
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
-// X[i + 256 m].  Uses buf for the two exchanges.
-__device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf, const float2* twA,
-                                        const float2* twB, int i)
+// X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
+// barrier: a buffer is rewritten only after the barrier that follows its last read.
+__device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf0, float2* buf1,
+                                        const float2* twA, const float2* twB, int i)
 {
-    pass_out<1>(u, buf, twA, twB, i);
+    pass_out<1>(u, buf0, twA, twB, i);
     __syncthreads();
-    load_in(u, buf, i);
+    load_in(u, buf0, i);
+    pass_out<16>(u, buf1, twA, twB, i);
     __syncthreads();
-    pass_out<16>(u, buf, twA, twB, i);
-    __syncthreads();
-    load_in(u, buf, i);
-    __syncthreads();
+    load_in(u, buf1, i);
     const int k = i;  // span 256: k = i, outputs at i + 256 m stay in this thread
 #pragma unroll
     for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], twiddle(twA, twB, j * k));
@@ -267,7 +266,7 @@ __device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf, const floa
 // ASYNC (rows 16-byte aligned, Nu % 4 == 0): the next row pair is fetched into a shared
 // staging buffer with cp.async while the current pair is transformed, hiding HBM latency.
 constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
-constexpr size_t kF4kSmem = sizeof(float2) * (4096 + 256) + sizeof(float2) * (256 + 16) +
+constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float2) * (256 + 16) +
                             sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage;
 
 template <bool ASYNC>
@@ -278,8 +277,9 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
 {
     using namespace f4k;
     extern __shared__ __align__(16) unsigned char fsm[];
-    float2* const buf = reinterpret_cast<float2*>(fsm);  // L + L/16 (padded)
-    float2* const twA = buf + (L + L / 16);                // 256
+    float2* const buf = reinterpret_cast<float2*>(fsm);  // 2 x (L + L/16) (padded)
+    float2* const bufB = buf + (L + L / 16);
+    float2* const twA = bufB + (L + L / 16);               // 256
     float2* const twB = twA + 256;                          // 16
     float* const Hs = reinterpret_cast<float*>(twB + 16);   // L/2 + 1 (2052 slots)
     float* const stage = Hs + 2052;                         // 2 rows
@@ -325,14 +325,16 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             float2 x = make_float2(0.f, 0.f);
             if (j < 8 && n < p.Nu) {
                 const float uh = ((float)n - p.cu) * p.Du;
-                x.x = (ASYNC ? eA[n] : __ldg(eA + n)) * (p.D / sqrtf(dA + uh * uh));
-                if (hasB) x.y = (ASYNC ? eB[n] : __ldg(eB + n)) * (p.D / sqrtf(dB + uh * uh));
+                // F_cos = D / sqrt(D^2 + uh^2 + vh^2); rsqrtf's <= 2 ulp error is far below the
+                // filter tolerance and saves the IEEE sqrt + divide sequences.
+                x.x = (ASYNC ? eA[n] : __ldg(eA + n)) * (p.D * rsqrtf(fmaf(uh, uh, dA)));
+                if (hasB) x.y = (ASYNC ? eB[n] : __ldg(eB + n)) * (p.D * rsqrtf(fmaf(uh, uh, dB)));
             }
             u[j] = x;
         }
-        __syncthreads();  // staging read and buf free: fetch the next pair while this one runs
+        __syncthreads();  // staging read and buffers free: fetch the next pair meanwhile
         prefetch(pr + gridDim.x);
-        fft4096(u, buf, twA, twB, i);
+        fft4096(u, buf, bufB, twA, twB, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -340,8 +342,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             const float h = Hs[f <= L / 2 ? f : L - f];
             u[m] = make_float2(u[m].x * h, -u[m].y * h);
         }
-        __syncthreads();
-        fft4096(u, buf, twA, twB, i);
+        fft4096(u, buf, bufB, twA, twB, i);  // buf's last reader was before bufB's barrier
         // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1.
         float* qA = p.out + rA * p.Nu;
         float* qB = p.out + rB * p.Nu;
