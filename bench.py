@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "kslab"],
+                    help="kslab forces the multi-GPU k-slab driver even at N=1")
     return ap.parse_args()
 
 
@@ -222,7 +224,7 @@ def run_ours(args, spec, rank, world, local_rank):
     vol = torch.empty((nk, spec.Ny, spec.Nx), device=dev, dtype=torch.float32)
     batch = 256
     Q = torch.empty((min(batch, nv), spec.Nv, spec.Nu), device=dev, dtype=torch.float32) \
-        if world == 1 else None
+        if (world == 1 and args.path == "auto") else None
 
     bp_events = []
 
@@ -251,7 +253,7 @@ def run_ours(args, spec, rank, world, local_rank):
         kslab_reconstruct(g, raw, vol, plan, rank, timings=timings if record else None)
         return 2 + world  # filter + one BP per source rank (+ NCCL)
 
-    step = step_single if world == 1 else step_multi
+    step = step_single if (world == 1 and args.path == "auto") else step_multi
 
     for _ in range(args.warmup):
         step(False)
@@ -299,7 +301,8 @@ def run_ours(args, spec, rank, world, local_rank):
     # memory and D2H of the volume inside the timed region, every step.
     e2e = None
     if not args.no_e2e and world == 1:
-        del Q
+        if Q is not None:
+            del Q
         torch.cuda.empty_cache()
         raw_h = torch.empty(raw.shape, dtype=torch.float32, pin_memory=True)
         raw_h.copy_(raw)
@@ -347,8 +350,11 @@ def run_ours(args, spec, rank, world, local_rank):
         "config": {"workload": spec.name, "config_id": args.config,
                    "Np": spec.Np, "Nu": spec.Nu, "Nv": spec.Nv,
                    "volume": [spec.Nx, spec.Ny, spec.Nz],
-                   "parallelism": f"k-slab x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs (32 GiB) and volume far larger than the 126 MB L2; no flush"},
+                   "parallelism": f"k-slab x{world}" if (world > 1 or args.path == "kslab")
+                   else "single GPU",
+                   "l2": f"projections ({4 * spec.Np * spec.Nu * spec.Nv / 2**30:.0f} GiB) and "
+                         f"volume ({4 * spec.Nx * spec.Ny * spec.Nz / 2**30:.0f} GiB) far larger "
+                         "than the 126 MB L2; no flush"},
         "bp_gups": bp_gups,
         "bp_share_of_step": bp_share,
         "roofline": {"bound": "smem", "achieved": achieved_gbs, "peak": peak_gbs,
@@ -362,7 +368,7 @@ def run_ours(args, spec, rank, world, local_rank):
         "gpu_launches": launches,
         "cpu_baseline": cpu,
     }
-    if world > 1:
+    if timings:
         out["stage_ms"] = timings
     print(json.dumps(out), flush=True)
 

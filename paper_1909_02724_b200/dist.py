@@ -131,15 +131,17 @@ def kslab_reconstruct(g, raw_local, vol_slab, plan: SlabPlan, rank: int, group=N
     ex = plan_exchange(g, plan, rank)
     n_local = raw_local.shape[0]
     Nu = g.Nu
-    send_parts = [Q[:, lo:hi + 1, :].reshape(-1) for (lo, hi) in ex.send]
-    send_sizes = [p.numel() for p in send_parts]
     recv_sizes = [plan.views(r)[1] * _rows(ex.recv[r]) * Nu for r in range(plan.world)]
-    send_buf = torch.cat(send_parts) if sum(send_sizes) else Q.new_empty(0)
-    recv_buf = Q.new_empty(sum(recv_sizes))
+    send_sizes = [n_local * _rows(b) * Nu for b in ex.send]
     if plan.world > 1:
+        send_parts = [Q[:, lo:hi + 1, :].reshape(-1) for (lo, hi) in ex.send]
+        send_buf = torch.cat(send_parts) if sum(send_sizes) else Q.new_empty(0)
+        recv_buf = Q.new_empty(sum(recv_sizes))
         dist.all_to_all_single(recv_buf, send_buf, recv_sizes, send_sizes, group=group)
-    else:
-        recv_buf.copy_(send_buf)
+        del send_buf
+    else:  # one rank: the band is read in place
+        lo, hi = ex.recv[0]
+        recv_buf = Q[:, lo:hi + 1, :].contiguous().reshape(-1) if _rows(ex.recv[0]) else Q.new_empty(0)
     if marks:
         marks[2].record()
     k0, nk = plan.slab(rank)
