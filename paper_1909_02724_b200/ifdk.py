@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libifdk.so")
+# IFDK_LIB may point at another build of the same library (A/B timing of kernel variants).
+LIB_PATH = os.environ.get("IFDK_LIB") or os.path.join(_HERE, "libifdk.so")
 
 IFDK_OK = 0
 STATUS_NAMES = {
