@@ -47,12 +47,10 @@ struct BPParams {
     int kb0;          // global k of chunk 0 (multiple of KC)
     int tiles_i;
     int box_w, box_h;
-    int raw_bytes;    // bytes of one raw box buffer (box_w x box_rows + slack, multiple of 128)
-    int box_rows;     // box_h rounded up to a multiple of 8 (rows allocated per buffer)
+    int raw_bytes;    // bytes of one raw box (multiple of 128)
     int vb;           // view batch of the two-level summation
     uint32_t neg_magic;  // -0x4B000000 * P2 * 8 mod 2^32 (see accumulate_view_smem)
     int pair;            // PAIR walk (dv < 1 everywhere)
-    int hook;            // rewrite the next view's patch inside the update loop
     int accumulate;
 };
 
@@ -354,7 +352,7 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, in
     }
 }
 
-template <int KC, int P2, bool TMA, bool PAIR, bool NARROW>
+template <int KC, int P2, bool TMA, bool PAIR>
 __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap)
 {
@@ -382,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
 
     // raw box of view t: smem + (t & 1) raw_bytes; pair patch of view t: pair0 + (t & 1) box_h P2
     float2* const pair0 = reinterpret_cast<float2*>(smem + 2 * p.raw_bytes);
-    Meta* const meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_rows * P2);  // ring of kMetaRing
+    Meta* const meta = reinterpret_cast<Meta*>(pair0 + 2 * p.box_h * P2);  // ring of kMetaRing
     uint64_t* const mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
     const uint32_t tx_bytes = (uint32_t)(p.box_w * p.box_h * 4);
     // The tensor map must be addressed in param space (__grid_constant__): take its address
@@ -400,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     auto transform = [=](int t) {  // all threads: used part of the raw box -> (a, b - a) pairs
         const Meta& m = meta[t & (kMetaRing - 1)];
         const float* r = reinterpret_cast<const float*>(smem + (t & 1) * p.raw_bytes);
-        float2* q = pair0 + (t & 1) * p.box_rows * P2;
+        float2* q = pair0 + (t & 1) * p.box_h * P2;
         const int wp = m.w_need - 1, hn = m.h_need;
         if (p.box_w <= 32) {
             // One detector row per warp and iteration, one column per lane; b = a of lane+1.
@@ -480,33 +478,28 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
             // 8-slice group), the rest after.
             const bool nxt = t + 1 < n;
             int hn = 0, wp = 0;
+            const float* rbase = nullptr;
+            float2* qbase = nullptr;
             if (nxt) {
                 mbar_wait(&mbar[(t + 1) & 1], (uint32_t)(((t + 1) >> 1) & 1));
                 const Meta& mn = meta[(t + 1) & (kMetaRing - 1)];
                 if (!mn.fast) __trap();  // the host sizes the box from a conservative bound
                 hn = mn.h_need;
                 wp = mn.w_need - 1;
+                rbase = reinterpret_cast<const float*>(smem + ((t + 1) & 1) * p.raw_bytes);
+                qbase = pair0 + ((t + 1) & 1) * p.box_h * P2;
             }
-            // After the last view the hook rewrites stale data into the unused buffer with
-            // every store masked off (wp = 0).
-            const float* const rbase =
-                reinterpret_cast<const float*>(smem + ((t + 1) & 1) * p.raw_bytes) + lane;
-            float2* const qbase = pair0 + ((t + 1) & 1) * p.box_rows * P2 + lane;
-            const bool wr = lane < wp;
-            auto row = [&](int q) {  // transform row warp + 8 q of the next view, branch-free
-                if constexpr (NARROW) {
-                    if (p.hook) {
-                        const int rr = warp + (kThreads / 32) * q;
-                        // rows past box_rows would leave the buffer: read stays in the raw
-                        // buffer's slack-free range by clamping, the store is masked
-                        const int rc = min(rr, p.box_rows - 1);
-                        const float a = rbase[rc * p.box_w];
-                        const float b = __shfl_down_sync(0xffffffffu, a, 1);
-                        if (wr && rr < hn) qbase[rr * P2] = make_float2(a, b - a);
-                    }
+            const bool narrow = p.box_w <= 32;
+            const bool in_box = lane < p.box_w, wr = lane < wp;
+            auto row = [&](int q) {  // transform row warp + 8 q of the next view (narrow boxes)
+                const int rr = warp + (kThreads / 32) * q;
+                if (narrow && rr < hn) {
+                    const float a = in_box ? rbase[rr * p.box_w + lane] : 0.f;
+                    const float b = __shfl_down_sync(0xffffffffu, a, 1);
+                    if (wr) qbase[rr * P2 + lane] = make_float2(a, b - a);
                 }
             };
-            const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_rows * P2);
+            const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
             if (full)
                 accumulate_view_smem<KC, P2, true, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
                                                          kv0, kv1, row);
@@ -514,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
                 accumulate_view_smem<KC, P2, false, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
                                                           kv0, kv1, row);
             if (nxt) {
-                if (NARROW && p.hook) {
+                if (narrow) {
                     for (int q = KC / 8; warp + (kThreads / 32) * q < hn; ++q) row(q);
                 } else {
                     transform(t + 1);
@@ -557,13 +550,12 @@ ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, bool tma, dim3 g
 {
     cudaError_t e;
     if (tma) {
-        auto k = p.box_w <= 32 ? bp_kernel<KC, P2, true, PAIR, true>
-                               : bp_kernel<KC, P2, true, PAIR, false>;
+        auto k = bp_kernel<KC, P2, true, PAIR>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp)");
         k<<<grid, kThreads, smem, st>>>(p, map);
     } else {
-        auto k = bp_kernel<KC, P2, false, PAIR, false>;
+        auto k = bp_kernel<KC, P2, false, PAIR>;
         k<<<grid, kThreads, 0, st>>>(p, map);
     }
     e = cudaGetLastError();
@@ -646,10 +638,6 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
     p.pair = use_pair(g) ? 1 : 0;
-    {
-        const char* he = std::getenv("IFDK_BP_HOOK");
-        p.hook = (he && he[0] == '0') ? 0 : 1;
-    }
     int box_h = (int)std::ceil(hb) + 6 + p.pair;
     if (box_w < 8) box_w = 8;
     int P2 = 0;
@@ -663,10 +651,8 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     if (tma) {
         p.box_w = box_w;
         p.box_h = box_h;
-        p.box_rows = (box_h + 7) / 8 * 8;
-        p.raw_bytes = (box_w * p.box_rows * 4 + 32 * 4 + 127) / 128 * 128;
-        smem = 2 * (size_t)p.raw_bytes + 2 * sizeof(float2) * p.box_rows * P2 +
-               kMetaRing * sizeof(Meta) + 16;
+        p.raw_bytes = (box_w * box_h * 4 + 127) / 128 * 128;
+        smem = 2 * (size_t)p.raw_bytes + 2 * sizeof(float2) * box_h * P2 + kMetaRing * sizeof(Meta) + 16;
         cuuint64_t dims[3] = {(cuuint64_t)g->Nu, (cuuint64_t)n_rows, (cuuint64_t)n_views};
         cuuint64_t strides[2] = {(cuuint64_t)g->Nu * 4, (cuuint64_t)g->Nu * 4 * n_rows};
         cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
@@ -681,7 +667,6 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
         P2 = 24;
         p.box_w = p.box_h = 0;
         p.raw_bytes = 0;
-        p.box_rows = 0;
     }
     p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
     dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
