@@ -24,7 +24,10 @@
  *     data buffers are owned by the caller; the library never frees them.
  *     Pointers named *_dev are CUDA device pointers on the current device;
  *     pointers named *_host are host pointers.  Only ifdk_reconstruct and
- *     ifdk_reconstruct_host allocate (stream-ordered) scratch, freed before return.
+ *     ifdk_reconstruct_host allocate scratch: stream-ordered, from a memory pool
+ *     owned by the geometry that keeps its memory between calls (so repeated
+ *     reconstructions do not remap tens of GiB) and is released by
+ *     ifdk_geometry_destroy.
  *   - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy
  *     default stream).  Device work is enqueued asynchronously on it; the
  *     status reports argument and launch errors only.  Asynchronous faults
@@ -62,7 +65,7 @@ ifdk_status ifdk_geometry_create(int Nu, int Nv, int Nx, int Ny, int Nz, double 
                                  double Dx, double Dy, double Dz, double D, double d,
                                  double theta, ifdk_geometry** out);
 
-/* Free a geometry (NULL-safe) and the per-device tables it owns. */
+/* Free a geometry (NULL-safe), the per-device tables it owns and its scratch pool. */
 void ifdk_geometry_destroy(ifdk_geometry* g);
 
 /* P_s as a row-major 3x4 fp64 matrix (appendix; 3x4 per reading c-A1).
@@ -91,7 +94,9 @@ ifdk_status ifdk_filter(const ifdk_geometry* g, const float* raw_dev, float* fil
  * ([n_views][n_rows][Nu], device); those rows must cover ifdk_band_rows(k0,nk,s)
  * for every view, else SHAPE (a silently zero tap would corrupt the result).
  * Taps off the detector read 0 (reading c-A9).  accumulate = 0 overwrites the
- * slab, 1 adds to it.  Per-voxel summation is in view order, fp32, with the
+ * slab, 1 adds to it.  The fp64 P_s of the views ride in constant memory (the
+ * kernel's parameter space, <= 256 views per launch; longer ranges launch once
+ * per 256-view block of the global index, which leaves the result unchanged).  Per-voxel summation is in view order, fp32, with the
  * per-column invariants z, u, 1/z^2 and the k-walk base of v in fp64
  * (DESIGN.md "Numerics").
  * Errors: INVALID_ARGUMENT (NULL, accumulate not 0/1), SHAPE (slab outside

@@ -43,6 +43,33 @@ static ifdk_status check_band(const ifdk_geometry* g, long n_views, int v0, int 
     return IFDK_OK;
 }
 
+cudaError_t scratch_alloc(ifdk_geometry* g, void** ptr, size_t bytes, cudaStream_t st)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev >= 32) return cudaErrorInvalidDevice;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        auto& D = g->dev[dev];
+        if (!D.pool) {
+            // The default pool returns its memory to the driver at every synchronisation, so a
+            // 40 GiB scratch set would be remapped on every call; this one keeps it.
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.handleTypes = cudaMemHandleTypeNone;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if ((e = cudaMemPoolCreate(&D.pool, &props)) != cudaSuccess) return e;
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(D.pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        pool = D.pool;
+    }
+    return cudaMallocFromPoolAsync(ptr, bytes, pool, st);
+}
+
 }  // namespace ifdk
 
 using namespace ifdk;
@@ -105,9 +132,9 @@ extern "C" ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw
     const size_t view_elems = (size_t)g->Nv * g->Nu;
     const long batch = n_views < kViewBatch ? (n_views > 0 ? n_views : 1) : kViewBatch;
     float* Q = nullptr;
-    cudaError_t e = cudaMallocAsync(&Q, sizeof(float) * view_elems * batch, st);
+    cudaError_t e = scratch_alloc(const_cast<ifdk_geometry*>(g), (void**)&Q,
+                                  sizeof(float) * view_elems * batch, st);
     if (e != cudaSuccess) return fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(filtered scratch)");
-    int launches = 0;
     if (n_views == 0) s = launch_backproject(g, Q, 0, 0, 0, g->Nv, vol_dev, 0, g->Nz, 0, st);
     for (long b0 = 0; b0 < n_views && s == IFDK_OK; b0 += batch) {
         const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
@@ -115,10 +142,8 @@ extern "C" ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw
                           g->Nv, st);
         if (s != IFDK_OK) break;
         s = launch_backproject(g, Q, b0, nb, 0, g->Nv, vol_dev, 0, g->Nz, b0 > 0 ? 1 : 0, st);
-        launches += 2;
     }
     cudaFreeAsync(Q, st);
-    t_launches = launches;
     return s;
 }
 
@@ -148,11 +173,11 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
     }
     cudaEvent_t slab_done = nullptr;
     cudaEventCreateWithFlags(&slab_done, cudaEventDisableTiming);
-    e = cudaMallocAsync(&vol, sizeof(float) * vol_elems, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&buf[0], sizeof(float) * view_elems * batch, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&buf[1], sizeof(float) * view_elems * batch, st);
+    ifdk_geometry* gm = const_cast<ifdk_geometry*>(g);
+    e = scratch_alloc(gm, (void**)&vol, sizeof(float) * vol_elems, st);
+    if (e == cudaSuccess) e = scratch_alloc(gm, (void**)&buf[0], sizeof(float) * view_elems * batch, st);
+    if (e == cudaSuccess) e = scratch_alloc(gm, (void**)&buf[1], sizeof(float) * view_elems * batch, st);
     if (e != cudaSuccess) s = fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(reconstruct_host)");
-    int launches = 0;
     if (s == IFDK_OK) {
         cudaEvent_t ready;
         cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
@@ -179,11 +204,9 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
             cudaStreamWaitEvent(st, copied[q], 0);
             s = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb, 0, g->Nv, st);
             if (s != IFDK_OK) break;
-            ++launches;
             if (b + 1 < nbatches) {
                 s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vol, 0, g->Nz,
                                        b0 > 0 ? 1 : 0, st);
-                ++launches;
             } else {
                 // Last batch: back-project slab by slab and stream each finished slab to the
                 // host on `cp` while the next slab computes (slab starts on multiples of 64
@@ -194,7 +217,6 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
                     float* vs = vol + (size_t)k0 * g->Ny * g->Nx;
                     s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vs, k0, nk,
                                            b0 > 0 ? 1 : 0, st);
-                    ++launches;
                     cudaEventRecord(slab_done, st);
                     cudaStreamWaitEvent(cp, slab_done, 0);
                     e = cudaMemcpyAsync(vol_host + (size_t)k0 * g->Ny * g->Nx, vs,
@@ -226,7 +248,6 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
     }
     cudaEventDestroy(slab_done);
     cudaStreamDestroy(cp);
-    t_launches = launches;
     return s;
 }
 
@@ -238,6 +259,7 @@ extern "C" void ifdk_geometry_destroy(ifdk_geometry* g)
         if (d.tw) cudaFree(d.tw);
         if (d.twA) cudaFree(d.twA);
         if (d.twB) cudaFree(d.twB);
+        if (d.pool) cudaMemPoolDestroy(d.pool);  // deferred until outstanding frees complete
     }
     delete g;
 }

@@ -15,6 +15,11 @@
 //    c-A9) into a double-buffered raw box, then rewritten once into (Q[r][c], Q[r][c+1] -
 //    Q[r][c]) pairs so that each detector row costs one LDS.64 and one FMA per update.
 //    TMA for view t+3 is in flight while view t is accumulated.
+//  * P_s lives in constant memory: each launch carries the fp64 rows of its <= 256 views in
+//    a __grid_constant__ kernel parameter (param space = the constant bank), so no
+//    per-launch device allocation or host-to-device copy is needed.  Longer view ranges are
+//    split into launches at global multiples of 256 views, which are also flush points of
+//    the two-level summation, so the split does not change a bit.
 //  * Views are summed in order; every VB views (aligned to global view index) the register
 //    partial sums are added to the volume, a two-level summation.
 //  * A view whose patch does not fit the box (never for the five configs) is accumulated
@@ -35,8 +40,17 @@ namespace {
 
 constexpr int kTI = 16, kTJ = 16, kThreads = 256;
 
+// Views per launch: their projection matrices ride in the kernel's parameter space
+// (20 KB of the 32 KB parameter limit).  A multiple of the summation batch vb = 128.
+constexpr int kMaxViewsPerLaunch = 256;
+
+// The used entries of P_s (P[0][2] = P[2][2] = 0, Theorems 2-3):
+// P00 P01 P03 | P10 P11 P12 P13 | P20 P21 P23
+struct PTable {
+    double P[kMaxViewsPerLaunch][10];
+};
+
 struct BPParams {
-    const double* P;  // [n_views][10]: P00 P01 P03 | P10 P11 P12 P13 | P20 P21 P23
     const float* Q;   // band [n_views][n_rows][Nu]
     float* vol;       // slab [nk][Ny][Nx]
     long n_views;
@@ -308,17 +322,16 @@ __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i
 // 8 warps compute the boxes of the next 8 views together, so no warp straggles at the barrier.
 constexpr int kMetaRing = 16;
 
-__device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, int i_hi, int j_lo,
-                              int j_hi, int kb, int kv0, int kv1)
+__device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, int t, int i_lo,
+                              int i_hi, int j_lo, int j_hi, int kb, int kv0, int kv1)
 {
     const int lane = threadIdx.x & 31;
     const int corner = lane & 3;
-    const double* Pg = p.P + (long)t * 10;
     double P[10];
 #pragma unroll
-    for (int q = 0; q < 10; ++q) P[q] = __ldg(Pg + q);
+    for (int q = 0; q < 10; ++q) P[q] = Pc[q];  // constant bank, warp-uniform address
     Meta* m = &ring[t & (kMetaRing - 1)];
-    if (lane < 10) m->P[lane] = __ldg(Pg + lane);
+    if (lane < 10) m->P[lane] = Pc[lane];
     const double ci = (corner & 1) ? i_hi : i_lo;
     const double cj = (corner & 2) ? j_hi : j_lo;
     const ColInv c = column_invariants(P, ci, cj, (double)kb);
@@ -354,7 +367,8 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, int t, int i_lo, in
 
 template <int KC, int P2, bool TMA, bool PAIR>
 __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
-    bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap)
+    bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
+              const __grid_constant__ PTable pt)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -387,6 +401,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     // here, in the kernel body, never through a by-reference lambda capture (which would copy
     // it to local memory, an illegal TMA operand).
     const CUtensorMap* const tmap_ptr = &tmap;
+    const PTable* const ptab = &pt;  // same rule: the lambdas must not copy the 20 KB table
 
     auto issue = [=](int t) {  // one thread: TMA of view t's box into raw buffer t & 1
         const Meta& m = meta[t & (kMetaRing - 1)];
@@ -427,7 +442,9 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
         }
     };
     auto metas = [=](int t0) {  // all warps: boxes of views t0 .. t0+7
-        if (t0 + warp < n) compute_meta1(meta, p, t0 + warp, i_lo, i_hi, j_lo, j_hi, kb, kv0, kv1);
+        if (t0 + warp < n)
+            compute_meta1(meta, p, ptab->P[t0 + warp], t0 + warp, i_lo, i_hi, j_lo, j_hi, kb, kv0,
+                          kv1);
     };
 
     if (TMA) {
@@ -469,7 +486,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
             v_org = m.v_org;
         } else {
 #pragma unroll
-            for (int q = 0; q < 10; ++q) Pr[q] = __ldg(p.P + (long)t * 10 + q);
+            for (int q = 0; q < 10; ++q) Pr[q] = ptab->P[t][q];
         }
         const ThreadInv ti = split(column_invariants(Pr, di, dj, dkb));
         if constexpr (TMA) {
@@ -545,18 +562,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 }
 
 template <int KC, int P2, bool PAIR>
-ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, bool tma, dim3 grid, size_t smem,
-                     cudaStream_t st)
+ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, const PTable& pt, bool tma,
+                     dim3 grid, size_t smem, cudaStream_t st)
 {
     cudaError_t e;
     if (tma) {
         auto k = bp_kernel<KC, P2, true, PAIR>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp)");
-        k<<<grid, kThreads, smem, st>>>(p, map);
+        k<<<grid, kThreads, smem, st>>>(p, map, pt);
     } else {
         auto k = bp_kernel<KC, P2, false, PAIR>;
-        k<<<grid, kThreads, 0, st>>>(p, map);
+        k<<<grid, kThreads, 0, st>>>(p, map, pt);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "bp_kernel launch");
@@ -588,36 +605,26 @@ int choose_kc(const ifdk_geometry* g)
 
 }  // namespace
 
-ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
-                               int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
-                               cudaStream_t st)
+namespace {
+
+// One launch over views s0 .. s0+n_views-1 (n_views <= kMaxViewsPerLaunch).
+ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n_views, int v0,
+                         int n_rows, float* vol, int k0, int nk, int accumulate, cudaStream_t st)
 {
-    if (n_views == 0) {
-        if (!accumulate) {
-            cudaError_t e =
-                cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nk * g->Ny * g->Nx, st);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
-        }
-        return IFDK_OK;
-    }
-    // Per-view projection matrices (fp64) for the device.
-    std::vector<double> Ph((size_t)n_views * 10);
+    // Per-view projection matrices (fp64), passed in the kernel's parameter space.
+    PTable pt;
     for (long t = 0; t < n_views; ++t) {
         double P[12];
         projection_matrix(g, s0 + t, P);
-        double* o = &Ph[(size_t)t * 10];
+        double* o = pt.P[t];
         o[0] = P[0]; o[1] = P[1]; o[2] = P[3];
         o[3] = P[4]; o[4] = P[5]; o[5] = P[6]; o[6] = P[7];
         o[7] = P[8]; o[8] = P[9]; o[9] = P[11];
     }
-    double* Pd = nullptr;
-    cudaError_t e = cudaMallocAsync(&Pd, Ph.size() * sizeof(double), st);
-    if (e != cudaSuccess) return fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(P table)");
-    e = cudaMemcpyAsync(Pd, Ph.data(), Ph.size() * sizeof(double), cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(P table)");
+    for (long t = n_views; t < kMaxViewsPerLaunch; ++t)
+        for (int q = 0; q < 10; ++q) pt.P[t][q] = 0.0;
 
     BPParams p{};
-    p.P = Pd;
     p.Q = Q;
     p.vol = vol;
     p.n_views = n_views;
@@ -673,28 +680,59 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
     ifdk_status s;
     if (p.pair && KC == 64) {
         switch (P2) {
-            case 24: s = launch_t<64, 24, true>(p, map, tma, grid, smem, st); break;
-            case 40: s = launch_t<64, 40, true>(p, map, tma, grid, smem, st); break;
-            case 56: s = launch_t<64, 56, true>(p, map, tma, grid, smem, st); break;
-            default: s = launch_t<64, 72, true>(p, map, tma, grid, smem, st); break;
+            case 24: s = launch_t<64, 24, true>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<64, 40, true>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<64, 56, true>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<64, 72, true>(p, map, pt, tma, grid, smem, st); break;
         }
     } else if (p.pair) {
         switch (P2) {
-            case 24: s = launch_t<32, 24, true>(p, map, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40, true>(p, map, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56, true>(p, map, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72, true>(p, map, tma, grid, smem, st); break;
+            case 24: s = launch_t<32, 24, true>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40, true>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56, true>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72, true>(p, map, pt, tma, grid, smem, st); break;
         }
     } else {
         switch (P2) {
-            case 24: s = launch_t<32, 24, false>(p, map, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40, false>(p, map, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56, false>(p, map, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72, false>(p, map, tma, grid, smem, st); break;
+            case 24: s = launch_t<32, 24, false>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40, false>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56, false>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72, false>(p, map, pt, tma, grid, smem, st); break;
         }
     }
-    cudaFreeAsync(Pd, st);
     return s;
+}
+
+}  // namespace
+
+ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
+                               int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
+                               cudaStream_t st)
+{
+    if (n_views == 0) {
+        if (!accumulate) {
+            cudaError_t e =
+                cudaMemsetAsync(vol, 0, sizeof(float) * (size_t)nk * g->Ny * g->Nx, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+        }
+        return IFDK_OK;
+    }
+    // Launches end at global view indices that are multiples of kMaxViewsPerLaunch (and so of
+    // the summation batch): every voxel sees the same sums in the same order as one launch.
+    const size_t view_elems = (size_t)n_rows * g->Nu;
+    long t = 0;
+    while (t < n_views) {
+        const long s = s0 + t;
+        long stop = (s >= 0 ? s / kMaxViewsPerLaunch + 1 : -((-s - 1) / kMaxViewsPerLaunch))
+                    * kMaxViewsPerLaunch;  // next multiple strictly above s
+        long n = stop - s;
+        if (n > n_views - t) n = n_views - t;
+        ifdk_status r = launch_range(g, Q + (size_t)t * view_elems, s, n, v0, n_rows, vol, k0, nk,
+                                     (accumulate || t > 0) ? 1 : 0, st);
+        if (r != IFDK_OK) return r;
+        t += n;
+    }
+    return IFDK_OK;
 }
 
 }  // namespace ifdk

@@ -27,6 +27,9 @@ struct ifdk_geometry {
         float2* tw = nullptr;
         float2* twA = nullptr;  // w^(16 a), a < 256 (length-4096 kernel)
         float2* twB = nullptr;  // w^b, b < 16
+        // stream-ordered pool for ifdk_reconstruct* scratch; keeps its memory between calls
+        // (release threshold = max) and is destroyed with the geometry
+        cudaMemPool_t pool = nullptr;
     } dev[32];
     std::mutex mu;
 };
@@ -37,6 +40,9 @@ namespace ifdk {
 ifdk_status fail(ifdk_status st, const std::string& msg);
 ifdk_status cuda_fail(cudaError_t e, const char* what);
 void count_launch(int n = 1);
+
+// Scratch from the geometry's per-device pool (api.cu); freed with cudaFreeAsync.
+cudaError_t scratch_alloc(ifdk_geometry* g, void** ptr, size_t bytes, cudaStream_t st);
 
 // geometry.cpp
 void projection_matrix(const ifdk_geometry* g, long s, double P[12]);

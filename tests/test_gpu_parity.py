@@ -175,6 +175,30 @@ def test_bp_view_split_accumulate_matches(torch_cuda):
     assert_parity(two.cpu().numpy(), one.cpu().numpy(), 1e-6, 1e-5, "view split")
 
 
+def test_bp_long_unaligned_view_range(torch_cuda):
+    """600 views from s0 = 100: the library launches per 256-view block of the global index
+    (P_s in the kernel's constant parameter space).  One call equals the oracle and is
+    bitwise equal to calls cut at other multiples of the 128-view summation batch."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    spec = _spec(900, 40, 40, 24, 20, 28)
+    g = Geometry.from_spec(spec)
+    s0, n = 100, 600
+    Qn = _oracle_Q32(spec, _phantom_E(spec, s0, n))
+    Q = torch.from_numpy(Qn).cuda()
+    one = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+    ifdk_backproject(g, Q, s0, one)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=s0)
+    assert_parity(one.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp 600 views from s0=100")
+    for cuts in ((100, 128, 384, 700), (100, 640, 700), (100, 256, 512, 640, 700)):
+        part = torch.empty_like(one)
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            ifdk_backproject(g, Q[a - s0:b - s0].contiguous(), a, part, accumulate=a > s0)
+        assert torch.equal(part, one), cuts
+
+
 def test_bp_band_not_covering_is_shape_error(torch_cuda):
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, IfdkError, ifdk_backproject
