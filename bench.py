@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the projection-split measurement at N > 1")
     ap.add_argument("--path", default="auto", choices=["auto", "kslab"],
                     help="kslab forces the multi-GPU k-slab driver even at N=1")
     return ap.parse_args()
@@ -199,6 +201,17 @@ def run_reference(args, spec, rank, world):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def _max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, spec, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -206,34 +219,41 @@ def run_ours(args, spec, rank, world, local_rank):
     import synth
     from paper_1909_02724_b200 import (Geometry, ifdk_backproject, ifdk_filter,
                                        ifdk_reconstruct_host, last_launch_count)
-    from paper_1909_02724_b200.dist import SlabPlan, kslab_reconstruct
+    from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct, kslab_reconstruct_host,
+                                            projection_split_reconstruct)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     g = Geometry.from_spec(spec)
     plan = SlabPlan(world, spec.Nz, spec.Np)
-    vs0, nv = plan.views(rank)
     k0, nk = plan.slab(rank)
     stream = torch.cuda.current_stream()
+    use_kslab = world > 1 or args.path == "kslab"
 
-    # Inputs: this rank's raw views, analytic projections generated on the device.
-    raw = torch.empty((nv, spec.Nv, spec.Nu), device=dev, dtype=torch.float32)
+    # Inputs: this rank's raw views (all of them on one GPU; its 128-view blocks under the
+    # k-slab split), analytic projections generated on the device.
+    blocks = plan.local_views(rank) if use_kslab else [(0, spec.Np)]
+    n_local = sum(n for _, n in blocks)
+    raw = torch.empty((n_local, spec.Nv, spec.Nu), device=dev, dtype=torch.float32)
     ell = synth.default_ellipsoids(spec)
-    synth.project_gpu(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta, ell, vs0,
-                      nv, 0, spec.Nv, raw.data_ptr(), stream.cuda_stream)
+    off = 0
+    for s0, n in blocks:
+        synth.project_gpu(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta, ell,
+                          s0, n, 0, spec.Nv, raw[off:off + n].data_ptr(), stream.cuda_stream)
+        off += n
     vol = torch.empty((nk, spec.Ny, spec.Nx), device=dev, dtype=torch.float32)
     batch = 256
-    Q = torch.empty((min(batch, nv), spec.Nv, spec.Nu), device=dev, dtype=torch.float32) \
-        if (world == 1 and args.path == "auto") else None
+    Q = torch.empty((min(batch, n_local), spec.Nv, spec.Nu), device=dev, dtype=torch.float32) \
+        if not use_kslab else None
 
     bp_events = []
 
     def step_single(record):
-        """World 1: per 256-view batch, ifdk_filter then ifdk_backproject (what
+        """One GPU: per 256-view batch, ifdk_filter then ifdk_backproject (what
         ifdk_reconstruct does), with CUDA events around every BP launch."""
         launches = 0
-        for b0 in range(0, nv, batch):
-            nb = min(batch, nv - b0)
+        for b0 in range(0, n_local, batch):
+            nb = min(batch, n_local - b0)
             q = Q[:nb]
             ifdk_filter(g, raw[b0:b0 + nb], q)
             launches += last_launch_count()
@@ -248,12 +268,23 @@ def run_ours(args, spec, rank, world, local_rank):
         return launches
 
     timings = {}
+    counter = [0]
+
+    def f_fn(r, out):
+        ifdk_filter(g, r, out)
+        counter[0] += last_launch_count()
+
+    def b_fn(Qb, s0, v, kk0, v0, acc):
+        ifdk_backproject(g, Qb, s0, v, k0=kk0, v0=v0, accumulate=acc)
+        counter[0] += last_launch_count()
 
     def step_multi(record):
-        kslab_reconstruct(g, raw, vol, plan, rank, timings=timings if record else None)
-        return 2 + world  # filter + one BP per source rank (+ NCCL)
+        counter[0] = 0
+        kslab_reconstruct(g, raw, vol, plan, rank, filter_fn=f_fn, bp_fn=b_fn,
+                          timings=timings if record else None, force_exchange=True)
+        return counter[0]
 
-    step = step_single if (world == 1 and args.path == "auto") else step_multi
+    step = step_multi if use_kslab else step_single
 
     for _ in range(args.warmup):
         step(False)
@@ -269,18 +300,18 @@ def run_ours(args, spec, rank, world, local_rank):
         dist.barrier()
     t_start.record()
     launches = 0
+    stage = {}
     for _ in range(args.steps):
         launches += step(True)
+        for k, v in timings.items():
+            stage[k] = stage.get(k, 0.0) + v
     t_end.record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = t_start.elapsed_time(t_end) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = _max_over_ranks(t_start.elapsed_time(t_end) / args.steps, world, dev)
+    stage = {k: v / args.steps for k, v in stage.items()}
 
     # Dominant kernel: the back-projection; algorithmic smem bytes / its launch duration.
     if bp_events:
@@ -289,38 +320,80 @@ def run_ours(args, spec, rank, world, local_rank):
         bp_s = sum(dur) / len(dur)
         upd_per_launch = sum(n_updates) / len(n_updates)
         bp_share = sum(dur) / (ms / 1e3 * args.steps)
-    else:
-        bp_s = timings.get("bp_ms", float("nan")) / 1e3
-        upd_per_launch = spec.Nx * spec.Ny * nk * spec.Np
-        bp_share = bp_s / (ms / 1e3)
+    else:  # k-slab driver: per-round BP spans (plan.world launches of 128 views each)
+        bp_s = stage.get("bp_ms", float("nan")) / 1e3 / max(plan.n_rounds, 1)
+        upd_per_launch = spec.Nx * spec.Ny * nk * spec.Np / max(plan.n_rounds, 1)
+        bp_share = stage.get("bp_ms", float("nan")) / ms
     achieved_gbs = SMEM_BYTES_PER_UPDATE * upd_per_launch / bp_s / 1e9
     peak_gbs = N_SM * SMEM_B_PER_CLK_PER_SM * 1965e6 / 1e9  # at the max SM clock
     bp_gups = upd_per_launch / bp_s / 2 ** 30
+    if use_kslab and stage.get("wall_ms"):
+        # delta: sum of the stage times over the wall time of the pipelined step
+        stage["delta"] = (stage.get("filter_pack_ms", 0) + stage.get("bp_ms", 0)) / stage["wall_ms"]
 
-    # End to end through the public host API: H2D of the raw projections from pinned host
-    # memory and D2H of the volume inside the timed region, every step.
+    # End to end through the public API: H2D of the raw projections from pinned host memory
+    # and D2H of the volume inside the timed region, every step.
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         if Q is not None:
             del Q
         torch.cuda.empty_cache()
         raw_h = torch.empty(raw.shape, dtype=torch.float32, pin_memory=True)
         raw_h.copy_(raw)
-        del raw
-        torch.cuda.empty_cache()
         vol_h = torch.empty(vol.shape, dtype=torch.float32, pin_memory=True)
         n_e2e = args.e2e_steps if args.e2e_steps is not None else min(args.steps, 2)
-        ifdk_reconstruct_host(g, raw_h, vol_h)  # warm-up (allocator, tables)
-        t0 = time.perf_counter()
-        for _ in range(n_e2e):
-            ifdk_reconstruct_host(g, raw_h, vol_h)
-        e2e_s = (time.perf_counter() - t0) / n_e2e
+        if not use_kslab:
+            del raw
+            torch.cuda.empty_cache()
+            ifdk_reconstruct_host(g, raw_h, vol_h)  # warm-up (scratch pool, tables)
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                ifdk_reconstruct_host(g, raw_h, vol_h)
+            e2e_s = (time.perf_counter() - t0) / n_e2e
+            api = "ifdk_reconstruct_host (C ABI)"
+        else:
+            kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True)
+            torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(n_e2e):
+                kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True)
+            torch.cuda.synchronize()
+            e2e_s = _max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
+            api = "dist.kslab_reconstruct_host (per rank: H2D of its blocks, D2H of its slab)"
+        h2d = _max_over_ranks(float(raw_h.numel() * 4), world, dev) * world
+        d2h = _max_over_ranks(float(vol_h.numel() * 4), world, dev) * world
         e2e = {"value": gups(spec, e2e_s), "unit": "GUPS", "seconds": e2e_s,
-               "h2d_bytes_per_step": raw_h.numel() * 4, "d2h_bytes_per_step": vol_h.numel() * 4,
-               "steps": n_e2e}
-    elif world > 1:
-        e2e = {"value": None, "unit": "GUPS", "note": "host API e2e measured at N=1 only",
-               "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "steps": n_e2e, "api": api}
+        del raw_h, vol_h
+
+    # The projection-split variant, measured against the slab split in the same run.
+    variants = {}
+    if world > 1 and not args.no_variants and spec.Nz % world == 0:
+        torch.cuda.empty_cache()
+        need = 4 * (spec.Nz * spec.Ny * spec.Nx + n_local * spec.Nv * spec.Nu)
+        free = torch.cuda.mem_get_info(dev)[0]
+        ok = _max_over_ranks(0.0 if free > 1.05 * need else 1.0, world, dev) == 0.0
+        if ok:
+            ps = torch.empty((spec.Nz // world, spec.Ny, spec.Nx), device=dev)
+            projection_split_reconstruct(g, raw, blocks, ps, world)  # warm-up
+            tm = {}
+            torch.cuda.synchronize()
+            dist.barrier()
+            projection_split_reconstruct(g, raw, blocks, ps, world, timings=tm)
+            pms = _max_over_ranks(tm["wall_ms"], world, dev)
+            same = (k0, nk) == (rank * spec.Nz // world, spec.Nz // world)
+            dmax = float((ps - vol).abs().max()) if same else float("nan")
+            vmax = _max_over_ranks(float(vol.abs().max()), world, dev)
+            variants["projection_split"] = {
+                "value": gups(spec, pms / 1e3), "unit": "GUPS", "ms_per_step": pms,
+                "reduce_scatter_ms": _max_over_ranks(tm["reduce_scatter_ms"], world, dev),
+                "max_abs_diff_vs_kslab_rel": _max_over_ranks(dmax, world, dev) / vmax}
+            del ps
+        else:
+            variants["projection_split"] = {"skipped": "full partial volume does not fit"}
 
     if rank != 0:
         return
@@ -350,8 +423,8 @@ def run_ours(args, spec, rank, world, local_rank):
         "config": {"workload": spec.name, "config_id": args.config,
                    "Np": spec.Np, "Nu": spec.Nu, "Nv": spec.Nv,
                    "volume": [spec.Nx, spec.Ny, spec.Nz],
-                   "parallelism": f"k-slab x{world}" if (world > 1 or args.path == "kslab")
-                   else "single GPU",
+                   "parallelism": f"k-slab x{world} (pipelined 128-view rounds, NCCL band "
+                                  "all-to-all)" if use_kslab else "single GPU",
                    "l2": f"projections ({4 * spec.Np * spec.Nu * spec.Nv / 2**30:.0f} GiB) and "
                          f"volume ({4 * spec.Nx * spec.Ny * spec.Nz / 2**30:.0f} GiB) far larger "
                          "than the 126 MB L2; no flush"},
@@ -368,8 +441,10 @@ def run_ours(args, spec, rank, world, local_rank):
         "gpu_launches": launches,
         "cpu_baseline": cpu,
     }
-    if timings:
-        out["stage_ms"] = timings
+    if stage:
+        out["stage_ms"] = stage
+    if variants:
+        out["variants"] = variants
     print(json.dumps(out), flush=True)
 
 
@@ -384,7 +459,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, spec, rank, world)
         return
-    if world > 1:
+    # Under torchrun the process group exists even at N = 1 when the k-slab driver is forced,
+    # so that its NCCL exchange runs on the pipeline's streams.
+    use_pg = world > 1 or (args.path == "kslab" and "MASTER_ADDR" in os.environ)
+    if use_pg:
         import torch
         import torch.distributed as dist
 
@@ -393,7 +471,7 @@ def main():
     try:
         run_ours(args, spec, rank, world, local_rank)
     finally:
-        if world > 1:
+        if use_pg:
             import torch.distributed as dist
 
             dist.destroy_process_group()

@@ -3,29 +3,39 @@
 Two decompositions of the paper's R x C rank grid on one node:
 
 * k-slab split (R = P, C = 1; primary).  Rank r owns the volume slab
-  k in [kb[r], kb[r+1]) and the raw views [vb[r], vb[r+1]).  It filters its own
-  views (Alg. alg:filter is row-separable), then one all-to-all sends to every
-  rank h only the detector row band slab h projects onto (ifdk_band_rows), the
-  NVLink analogue of the paper's per-projection MPI_Allgather cut
-  down to the rows actually used.  Each rank then back-projects all views, in
-  global view order, into its slab.  Slab starts are multiples of the kernel's
-  64-slice chunk and view blocks are multiples of its 128-view summation batch,
-  so the result is bitwise identical to one GPU.
+  k in [kb[r], kb[r+1]) (slab starts are multiples of the BP kernel's 64-slice chunk).
+  Views are sharded for filtering in blocks of ``block`` views, dealt round-robin:
+  rank r owns blocks r, r + P, r + 2P, ...  Round t processes blocks tP .. tP+P-1, one
+  per rank, i.e. the consecutive global views tPB .. (t+1)PB-1:
+    filter (own block) -> pack the row band every slab needs (ifdk_band_rows)
+    -> one all-to-all of the bands (the NVLink analogue of the paper's per-projection
+       MPI_Allgather, cut down to the rows actually used)
+    -> back-project the P received blocks, in global view order, into the own slab.
+  Rounds are software-pipelined on CUDA streams (the paper's filter / exchange / BP
+  threads, as streams): filter + exchange of round t+1 overlap the
+  back-projection of round t.  Because blocks are multiples of the kernel's 128-view
+  summation batch and arrive in global order, every slab is bitwise identical to one GPU.
 * projection split (R = 1, C = P; variant).  Rank r back-projects its views
   into a full-size partial volume; a reduce-scatter (sum) of the contiguous
   k-slabs replaces the paper's single MPI_Reduce.  Needs a full
   volume per GPU, so it does not fit config 5.
+
+``kslab_reconstruct_host`` is the end-to-end form: raw blocks come from pinned host
+memory (H2D on a copy stream, one round ahead) and the finished slab goes back to the
+host in sub-slabs while the last round's back-projection continues.
 
 The compute callables default to libifdk (``ifdk_filter`` / ``ifdk_backproject``);
 tests inject the fp64 oracle to check the exchange logic on CPU with gloo.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+import contextlib
+from dataclasses import dataclass, field
 from typing import Callable, Optional
 
 KC = 64          # slab starts are multiples of the BP kernel k-chunk (32 or 64, backproject.cu)
 VIEW_BATCH = 128  # two-level summation batch of the BP kernel (BPParams.vb)
+D2H_SUBSLAB = 256  # slices per device-to-host piece of the end-to-end driver (multiple of KC)
 
 
 def _split(n: int, parts: int, quantum: int) -> list[int]:
@@ -43,27 +53,45 @@ def _split(n: int, parts: int, quantum: int) -> list[int]:
 
 @dataclass(frozen=True)
 class SlabPlan:
-    """Which slab and which views rank r owns (k-slab split)."""
+    """Which slab rank r owns, and which view blocks (k-slab split)."""
 
     world: int
     Nz: int
     Np: int
+    block: int = VIEW_BATCH
 
     @property
     def k_bounds(self) -> list[int]:
         return _split(self.Nz, self.world, KC)
 
-    @property
-    def v_bounds(self) -> list[int]:
-        return _split(self.Np, self.world, VIEW_BATCH)
-
     def slab(self, r: int) -> tuple[int, int]:
         kb = self.k_bounds
         return kb[r], kb[r + 1] - kb[r]
 
-    def views(self, r: int) -> tuple[int, int]:
-        vb = self.v_bounds
-        return vb[r], vb[r + 1] - vb[r]
+    @property
+    def n_blocks(self) -> int:
+        return (self.Np + self.block - 1) // self.block
+
+    @property
+    def n_rounds(self) -> int:
+        return (self.n_blocks + self.world - 1) // self.world
+
+    def block_views(self, b: int) -> tuple[int, int]:
+        """(first global view, count) of block b (count 0 past the end)."""
+        s0 = b * self.block
+        return s0, max(0, min(self.block, self.Np - s0))
+
+    def round_block(self, t: int, r: int) -> tuple[int, int]:
+        """The block rank r filters in round t."""
+        return self.block_views(t * self.world + r)
+
+    def local_views(self, r: int) -> list[tuple[int, int]]:
+        """Rank r's blocks (global first view, count) in local storage order."""
+        return [self.round_block(t, r) for t in range(self.n_rounds)
+                if self.round_block(t, r)[1] > 0]
+
+    def n_local(self, r: int) -> int:
+        return sum(n for _, n in self.local_views(r))
 
 
 def band_union(g, k0: int, nk: int, s0: int, n: int) -> tuple[int, int]:
@@ -78,121 +106,329 @@ def band_union(g, k0: int, nk: int, s0: int, n: int) -> tuple[int, int]:
     return lo, hi
 
 
+def _rows(b):
+    return max(b[1] - b[0] + 1, 0)
+
+
 @dataclass
 class Exchange:
-    """Row bands of one all-to-all: send[h] = (lo, hi) of my views for slab h;
-    recv[r] = (lo, hi) of rank r's views for my slab."""
+    """Row bands of one round's all-to-all: send[h] = (lo, hi) of my block for slab h;
+    recv[r] = (lo, hi) of rank r's block for my slab; views[r] = (s0, n) of r's block."""
 
     send: list[tuple[int, int]]
     recv: list[tuple[int, int]]
+    views: list[tuple[int, int]]
+    send_sizes: list[int] = field(default_factory=list)
+    recv_sizes: list[int] = field(default_factory=list)
 
 
-def plan_exchange(g, plan: SlabPlan, rank: int) -> Exchange:
-    s0, n = plan.views(rank)
+_EXCHANGE_CACHE: dict = {}
+
+
+def exchanges(g, plan: SlabPlan, rank: int) -> list[Exchange]:
+    """plan_exchange for every round (cached per geometry, plan and rank)."""
+    key = (g.Nu, g.Nv, g.Nx, g.Ny, g.Nz, g.Du, g.Dv, g.Dx, g.Dy, g.Dz, g.D, g.d, g.theta,
+           plan, rank)
+    if key not in _EXCHANGE_CACHE:
+        if len(_EXCHANGE_CACHE) > 64:
+            _EXCHANGE_CACHE.clear()
+        _EXCHANGE_CACHE[key] = [plan_exchange(g, plan, rank, t) for t in range(plan.n_rounds)]
+    return _EXCHANGE_CACHE[key]
+
+
+def plan_exchange(g, plan: SlabPlan, rank: int, t: int) -> Exchange:
+    """The bands of round t as seen by ``rank`` (both directions)."""
+    s0, n = plan.round_block(t, rank)
     send = []
     for h in range(plan.world):
         k0, nk = plan.slab(h)
         send.append(band_union(g, k0, nk, s0, n) if nk > 0 and n > 0 else (0, -1))
     k0, nk = plan.slab(rank)
-    recv = []
+    recv, views = [], []
     for r in range(plan.world):
-        rs0, rn = plan.views(r)
+        rs0, rn = plan.round_block(t, r)
+        views.append((rs0, rn))
         recv.append(band_union(g, k0, nk, rs0, rn) if nk > 0 and rn > 0 else (0, -1))
-    return Exchange(send, recv)
+    ex = Exchange(send, recv, views)
+    ex.send_sizes = [n * _rows(b) * g.Nu for b in send]
+    ex.recv_sizes = [views[r][1] * _rows(recv[r]) * g.Nu for r in range(plan.world)]
+    return ex
 
 
-def _rows(b):
-    return max(b[1] - b[0] + 1, 0)
+class _Streams:
+    """CUDA streams/events for the pipeline, or no-ops for CPU tensors (gloo tests)."""
+
+    def __init__(self, cuda: bool):
+        import torch
+
+        self.cuda = cuda
+        self.torch = torch
+        if cuda:
+            self.F = torch.cuda.Stream()  # filter + band packing (+ exchange issue)
+            self.B = torch.cuda.Stream()  # back-projection
+            self.C = torch.cuda.Stream()  # host copies
+        else:
+            self.F = self.B = self.C = None
+
+    def on(self, s):
+        return self.torch.cuda.stream(s) if self.cuda else contextlib.nullcontext()
+
+    def event(self, timing=False):
+        return self.torch.cuda.Event(enable_timing=timing) if self.cuda else None
+
+    def record(self, ev, s):
+        if ev is not None:
+            ev.record(s)
+
+    def wait(self, s, ev):
+        if ev is not None and s is not None:
+            s.wait_event(ev)
 
 
-def kslab_reconstruct(g, raw_local, vol_slab, plan: SlabPlan, rank: int, group=None,
-                      filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
-                      timings: Optional[dict] = None):
-    """k-slab FDK on one rank.  raw_local: [n_local][Nv][Nu] (views plan.views(rank));
-    vol_slab: [nk][Ny][Nx] (slab plan.slab(rank)), overwritten."""
-    import torch
-    import torch.distributed as dist
-
+def _default_fns(g, filter_fn, bp_fn):
     if filter_fn is None or bp_fn is None:
         from .ifdk import ifdk_backproject, ifdk_filter
 
         filter_fn = filter_fn or (lambda raw, out: ifdk_filter(g, raw, out))
         bp_fn = bp_fn or (lambda Q, s0, vol, k0, v0, acc: ifdk_backproject(
             g, Q, s0, vol, k0=k0, v0=v0, accumulate=acc))
-    ev = (lambda: torch.cuda.Event(enable_timing=True)) if raw_local.is_cuda else None
-    marks = [ev() for _ in range(4)] if (ev and timings is not None) else None
-    if marks:
-        marks[0].record()
-    Q = torch.empty_like(raw_local)
-    if raw_local.shape[0] > 0:
-        filter_fn(raw_local, Q)
-    if marks:
-        marks[1].record()
-    ex = plan_exchange(g, plan, rank)
-    n_local = raw_local.shape[0]
-    Nu = g.Nu
-    recv_sizes = [plan.views(r)[1] * _rows(ex.recv[r]) * Nu for r in range(plan.world)]
-    send_sizes = [n_local * _rows(b) * Nu for b in ex.send]
-    if plan.world > 1:
-        send_parts = [Q[:, lo:hi + 1, :].reshape(-1) for (lo, hi) in ex.send]
-        send_buf = torch.cat(send_parts) if sum(send_sizes) else Q.new_empty(0)
-        recv_buf = Q.new_empty(sum(recv_sizes))
-        dist.all_to_all_single(recv_buf, send_buf, recv_sizes, send_sizes, group=group)
-        del send_buf
-    else:  # one rank: the band is read in place
-        lo, hi = ex.recv[0]
-        recv_buf = Q[:, lo:hi + 1, :].contiguous().reshape(-1) if _rows(ex.recv[0]) else Q.new_empty(0)
-    if marks:
-        marks[2].record()
-    k0, nk = plan.slab(rank)
-    off = 0
-    first = True
-    for r in range(plan.world):
-        rs0, rn = plan.views(r)
-        lo, hi = ex.recv[r]
-        sz = recv_sizes[r]
-        if rn > 0 and sz > 0 and nk > 0:
-            band = recv_buf[off:off + sz].view(rn, hi - lo + 1, Nu)
-            bp_fn(band, rs0, vol_slab, k0, lo, not first)
-            first = False
-        off += sz
-    if first and nk > 0:
-        vol_slab.zero_()
-    if marks:
-        marks[3].record()
-        marks[3].synchronize()
-        timings["filter_ms"] = marks[0].elapsed_time(marks[1])
-        timings["exchange_ms"] = marks[1].elapsed_time(marks[2])
-        timings["bp_ms"] = marks[2].elapsed_time(marks[3])
-        timings["exchange_bytes_sent"] = 4 * sum(s for h, s in enumerate(send_sizes) if h != rank)
-    return vol_slab
+    return filter_fn, bp_fn
 
 
-def projection_split_reconstruct(g, raw_local, s0: int, vol_slab, world: int, group=None,
-                                 filter_fn: Optional[Callable] = None,
-                                 bp_fn: Optional[Callable] = None):
-    """Projection split: full partial volume per rank, then reduce-scatter (sum) of equal
-    contiguous k-slabs (Nz must be divisible by world).  vol_slab: [Nz/world][Ny][Nx]."""
+def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, timings,
+              raw_local=None, raw_host=None, vol_host=None, force_exchange=False):
     import torch
     import torch.distributed as dist
 
-    if filter_fn is None or bp_fn is None:
-        from .ifdk import ifdk_backproject, ifdk_filter
+    filter_fn, bp_fn = _default_fns(g, filter_fn, bp_fn)
+    world = plan.world
+    # exchange through the process group even at world size 1 (exercises the collective on
+    # the pipeline's streams; the band is then packed and "sent" to itself)
+    xchg = world > 1 or (force_exchange and dist.is_available() and dist.is_initialized())
+    k0, nk = plan.slab(rank)
+    cuda = vol_slab.is_cuda
+    S = _Streams(cuda)
+    dev = vol_slab.device
+    Nv, Nu = g.Nv, g.Nu
+    rounds = plan.n_rounds
+    exs = exchanges(g, plan, rank)
+    my_blocks = plan.local_views(rank)
+    offs, o = [], 0
+    for _, n in my_blocks:
+        offs.append(o)
+        o += n
+    B = plan.block
+    # Persistent double buffers (no allocator traffic across streams).
+    Qbuf = [torch.empty((B, Nv, Nu), device=dev) for _ in range(min(2, rounds))]
+    send_max = max([sum(e.send_sizes) for e in exs] + [1])
+    recv_max = max([sum(e.recv_sizes) for e in exs] + [1])
+    sendbuf = [torch.empty(send_max, device=dev) for _ in Qbuf] if xchg else None
+    recvbuf = [torch.empty(recv_max, device=dev) for _ in Qbuf] if xchg else None
+    stage = [torch.empty((B, Nv, Nu), device=dev) for _ in Qbuf] if raw_host is not None else None
 
-        filter_fn = filter_fn or (lambda raw, out: ifdk_filter(g, raw, out))
-        bp_fn = bp_fn or (lambda Q, s0_, vol, k0, v0, acc: ifdk_backproject(
-            g, Q, s0_, vol, k0=k0, v0=v0, accumulate=acc))
+    cur = torch.cuda.current_stream() if cuda else None
+    t_start = S.event(True)
+    S.record(t_start, cur)
+    for s in (S.F, S.B, S.C):
+        S.wait(s, t_start)
+    ev_bp_done = [None, None]
+    ev_filt_done = [None, None]
+    ev_h2d = [None, None]
+    f_marks, b_marks, c_marks = [], [], []
+
+    def h2d(t):  # round t's own raw block -> stage[t % 2] on the copy stream
+        if raw_host is None or t >= rounds or plan.round_block(t, rank)[1] == 0:
+            return
+        q = t % 2
+        n = plan.round_block(t, rank)[1]
+        bi = sum(1 for tt in range(t) if plan.round_block(tt, rank)[1] > 0)
+        with S.on(S.C):
+            S.wait(S.C, ev_filt_done[q])  # stage[q] free once filter(t-2) has read it
+            e0 = S.event(True)
+            S.record(e0, S.C)
+            stage[q][:n].copy_(raw_host[offs[bi]:offs[bi] + n], non_blocking=True)
+            ev_h2d[q] = S.event(True)
+            S.record(ev_h2d[q], S.C)
+            c_marks.append((e0, ev_h2d[q]))
+
+    h2d(0)
+    first_bp = True
+    bi = 0
+    for t in range(rounds):
+        q = t % 2
+        ex = exs[t]
+        s0, n = plan.round_block(t, rank)
+        h2d(t + 1)
+        with S.on(S.F):
+            # sendbuf[q] / recvbuf[q] / Qbuf[q] were last used by round t-2's BP
+            S.wait(S.F, ev_bp_done[q])
+            e0 = S.event(True)
+            S.record(e0, S.F)
+            if n > 0:
+                if raw_host is not None:
+                    S.wait(S.F, ev_h2d[q])
+                    src = stage[q][:n]
+                else:
+                    src = raw_local[offs[bi]:offs[bi] + n]
+                filter_fn(src, Qbuf[q][:n])
+                bi += 1
+            ev_filt_done[q] = S.event()
+            S.record(ev_filt_done[q], S.F)
+            work = None
+            if xchg:
+                if n > 0:
+                    off = 0
+                    for (lo, hi), sz in zip(ex.send, ex.send_sizes):
+                        if sz:
+                            sendbuf[q][off:off + sz].view(n, hi - lo + 1, Nu).copy_(
+                                Qbuf[q][:n, lo:hi + 1, :])
+                        off += sz
+                e1 = S.event(True)
+                S.record(e1, S.F)
+                f_marks.append((e0, e1))
+                work = dist.all_to_all_single(recvbuf[q][:sum(ex.recv_sizes)],
+                                              sendbuf[q][:sum(ex.send_sizes)],
+                                              ex.recv_sizes, ex.send_sizes, group=group,
+                                              async_op=True)
+            else:
+                e1 = S.event(True)
+                S.record(e1, S.F)
+                f_marks.append((e0, e1))
+            ev_ready = S.event()
+            S.record(ev_ready, S.F)
+        with S.on(S.B):
+            if work is not None:
+                work.wait()  # the BP stream waits for the collective
+            S.wait(S.B, ev_ready)
+            b0 = S.event(True)
+            S.record(b0, S.B)
+            last = t == rounds - 1
+            # the last round goes in sub-slabs so that finished slices leave for the host early
+            subs = [(k0, nk)]
+            if last and vol_host is not None and nk > D2H_SUBSLAB:
+                subs = [(a, min(D2H_SUBSLAB, k0 + nk - a)) for a in range(k0, k0 + nk, D2H_SUBSLAB)]
+            launched = False
+            for (a, m) in subs:
+                acc_first = first_bp
+                off = 0
+                for r in range(world):
+                    rs0, rn = ex.views[r]
+                    lo, hi = ex.recv[r]
+                    sz = ex.recv_sizes[r]
+                    if rn > 0 and sz > 0 and nk > 0:
+                        if xchg:
+                            band, v0 = recvbuf[q][off:off + sz].view(rn, hi - lo + 1, Nu), lo
+                        else:  # one rank: back-project straight from the filtered block
+                            band, v0 = Qbuf[q][:rn], 0
+                        bp_fn(band, rs0, vol_slab[a - k0:a - k0 + m], a, v0, not acc_first)
+                        acc_first = False
+                        launched = True
+                    off += sz
+                if last and acc_first:  # no view of the whole scan touches these slices
+                    vol_slab[a - k0:a - k0 + m].zero_()
+                if last and vol_host is not None and m > 0:
+                    ev = S.event()
+                    S.record(ev, S.B)
+                    with S.on(S.C):
+                        S.wait(S.C, ev)
+                        c0 = S.event(True)
+                        S.record(c0, S.C)
+                        vol_host[a - k0:a - k0 + m].copy_(vol_slab[a - k0:a - k0 + m],
+                                                          non_blocking=True)
+                        c1 = S.event(True)
+                        S.record(c1, S.C)
+                        c_marks.append((c0, c1))
+            if launched:
+                first_bp = False
+            b1 = S.event(True)
+            S.record(b1, S.B)
+            b_marks.append((b0, b1))
+            ev_bp_done[q] = S.event()
+            S.record(ev_bp_done[q], S.B)
+    if rounds == 0 and nk > 0:  # no views at all
+        vol_slab.zero_()
+        if vol_host is not None:
+            vol_host.copy_(vol_slab)
+    if cuda:
+        for s in (S.F, S.B, S.C):
+            cur.wait_stream(s)
+    t_end = S.event(True)
+    S.record(t_end, cur)
+    if timings is not None and cuda:
+        t_end.synchronize()
+        wall = t_start.elapsed_time(t_end)
+        tf = sum(a.elapsed_time(b) for a, b in f_marks)
+        tb = sum(a.elapsed_time(b) for a, b in b_marks)
+        tc = sum(a.elapsed_time(b) for a, b in c_marks)
+        timings.update({"wall_ms": wall, "filter_pack_ms": tf, "bp_ms": tb, "host_copy_ms": tc,
+                        "rounds": rounds,
+                        "exchange_bytes_sent": 4 * sum(sum(e.send_sizes) - e.send_sizes[rank]
+                                                       for e in exs) if xchg else 0})
+    return vol_slab
+
+
+def kslab_reconstruct(g, raw_local, vol_slab, plan: SlabPlan, rank: int, group=None,
+                      filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
+                      timings: Optional[dict] = None, force_exchange: bool = False):
+    """k-slab FDK on one rank.  raw_local: [plan.n_local(rank)][Nv][Nu], the rank's blocks
+    (plan.local_views(rank)) in order, device-resident; vol_slab: [nk][Ny][Nx] (slab
+    plan.slab(rank)), overwritten.  Enqueued on side streams that the current stream joins."""
+    return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
+                     raw_local=raw_local, force_exchange=force_exchange)
+
+
+def kslab_reconstruct_host(g, raw_host, vol_slab, vol_host, plan: SlabPlan, rank: int,
+                           group=None, filter_fn: Optional[Callable] = None,
+                           bp_fn: Optional[Callable] = None, timings: Optional[dict] = None,
+                           force_exchange: bool = False):
+    """End-to-end k-slab FDK on one rank: raw_host (pinned, the rank's blocks in order) is
+    copied block by block one round ahead; vol_slab (device scratch [nk][Ny][Nx]) is
+    streamed to vol_host (pinned) in sub-slabs during the last round."""
+    return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
+                     raw_host=raw_host, vol_host=vol_host, force_exchange=force_exchange)
+
+
+def projection_split_reconstruct(g, raw_local, blocks, vol_slab, world: int, group=None,
+                                 filter_fn: Optional[Callable] = None,
+                                 bp_fn: Optional[Callable] = None,
+                                 timings: Optional[dict] = None):
+    """Projection split: rank r filters and back-projects its own views (``blocks``: the
+    (first global view, count) runs stored in raw_local, in order) into a full partial volume,
+    then a reduce-scatter (sum) leaves it the contiguous k-slab r (Nz divisible by world).
+    vol_slab: [Nz/world][Ny][Nx].  Equal to one GPU up to fp32 summation order."""
+    import torch
+    import torch.distributed as dist
+
+    filter_fn, bp_fn = _default_fns(g, filter_fn, bp_fn)
     if g.Nz % world:
         raise ValueError("projection split needs Nz divisible by the world size")
+    cuda = vol_slab.is_cuda
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if (cuda and timings is not None) else None
+    if ev:
+        ev[0].record()
     Q = torch.empty_like(raw_local)
     full = raw_local.new_empty((g.Nz, g.Ny, g.Nx))
     if raw_local.shape[0] > 0:
         filter_fn(raw_local, Q)
-        bp_fn(Q, s0, full, 0, 0, False)
-    else:
+    off, first = 0, True
+    for s0, n in blocks:
+        if n > 0:
+            bp_fn(Q[off:off + n], s0, full, 0, 0, not first)
+            first = False
+        off += n
+    if first:
         full.zero_()
+    del Q
+    if ev:
+        ev[1].record()
     if world > 1:
         dist.reduce_scatter_tensor(vol_slab, full, op=dist.ReduceOp.SUM, group=group)
     else:
         vol_slab.copy_(full)
+    if ev:
+        ev[2].record()
+        ev[2].synchronize()
+        timings.update({"filter_bp_ms": ev[0].elapsed_time(ev[1]),
+                        "reduce_scatter_ms": ev[1].elapsed_time(ev[2]),
+                        "wall_ms": ev[0].elapsed_time(ev[2])})
     return vol_slab

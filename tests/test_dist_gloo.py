@@ -13,8 +13,8 @@ import torch.multiprocessing as mp
 import oracle
 import synth
 from paper_1909_02724_b200 import Geometry
-from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct, plan_exchange,
-                                        projection_split_reconstruct)
+from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct, kslab_reconstruct_host,
+                                        plan_exchange, projection_split_reconstruct)
 
 SPEC = synth.ConfigSpec("dist 36x40x36->24x20x40", 36, 40, 36, 24, 20, 40)
 
@@ -62,20 +62,27 @@ def _worker(rank, world, port, mode, out_q):
         g = Geometry.from_spec(SPEC)
         f, b = _oracle_fns(og)
         E, ref = _reference()
-        if mode == "kslab":
-            plan = SlabPlan(world, SPEC.Nz, SPEC.Np)
-            s0, n = plan.views(rank)
+        if mode in ("kslab", "kslab_host"):
+            # 8-view blocks: 5 blocks of 36 views, several pipelined rounds and a short last one
+            plan = SlabPlan(world, SPEC.Nz, SPEC.Np, block=8)
             k0, nk = plan.slab(rank)
+            mine = np.concatenate([E[s0:s0 + n] for s0, n in plan.local_views(rank)])
+            assert mine.shape[0] == plan.n_local(rank)
             vol = torch.empty((nk, SPEC.Ny, SPEC.Nx))
-            kslab_reconstruct(g, torch.from_numpy(E[s0:s0 + n].copy()), vol, plan, rank,
-                              filter_fn=f, bp_fn=b)
+            if mode == "kslab":
+                kslab_reconstruct(g, torch.from_numpy(mine), vol, plan, rank, filter_fn=f, bp_fn=b)
+            else:
+                host = torch.full((nk, SPEC.Ny, SPEC.Nx), float("nan"))
+                kslab_reconstruct_host(g, torch.from_numpy(mine), vol, host, plan, rank,
+                                       filter_fn=f, bp_fn=b)
+                assert torch.equal(host, vol)
         else:
             n = SPEC.Np // world
             s0 = rank * n
             k0, nk = rank * SPEC.Nz // world, SPEC.Nz // world
             vol = torch.empty((nk, SPEC.Ny, SPEC.Nx))
-            projection_split_reconstruct(g, torch.from_numpy(E[s0:s0 + n].copy()), s0, vol, world,
-                                         filter_fn=f, bp_fn=b)
+            projection_split_reconstruct(g, torch.from_numpy(E[s0:s0 + n].copy()), [(s0, n)], vol,
+                                         world, filter_fn=f, bp_fn=b)
         d = vol.numpy().astype(np.float64) - ref[k0:k0 + nk]
         out_q.put((rank, float(np.abs(d).max() / np.abs(ref).max())))
     except Exception as e:  # surface the failure in the parent
@@ -84,7 +91,8 @@ def _worker(rank, world, port, mode, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mode", [(2, "kslab"), (3, "kslab"), (2, "projsplit")])
+@pytest.mark.parametrize("world,mode", [(2, "kslab"), (3, "kslab"), (2, "kslab_host"),
+                                        (2, "projsplit")])
 def test_multi_rank_matches_single(world, mode):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -103,17 +111,30 @@ def test_multi_rank_matches_single(world, mode):
 def test_slab_plan_alignment_and_exchange_bands():
     for world in (1, 2, 4, 8):
         plan = SlabPlan(world, 2048, 2048)
-        kb, vb = plan.k_bounds, plan.v_bounds
-        assert kb[0] == 0 and kb[-1] == 2048 and vb[0] == 0 and vb[-1] == 2048
-        assert all(k % 64 == 0 for k in kb) and all(v % 128 == 0 for v in vb)
+        kb = plan.k_bounds
+        assert kb[0] == 0 and kb[-1] == 2048
+        assert all(k % 64 == 0 for k in kb)
         assert all(b > a for a, b in zip(kb[:-1], kb[1:]))
-    plan = SlabPlan(3, 40, 36)
+        # every view is owned exactly once, blocks start on the 128-view summation batch,
+        # and round t covers the consecutive views of blocks tP .. tP+P-1
+        views = sorted(v for r in range(world) for s0, n in plan.local_views(r)
+                       for v in range(s0, s0 + n))
+        assert views == list(range(2048))
+        assert all(s0 % 128 == 0 for r in range(world) for s0, _ in plan.local_views(r))
+        for t in range(plan.n_rounds):
+            blocks = [plan.round_block(t, r) for r in range(world)]
+            assert all(b[0] == blocks[0][0] + 128 * i for i, b in enumerate(blocks))
+    plan = SlabPlan(3, 40, 36, block=8)
     assert plan.k_bounds[-1] == 40 and sum(plan.slab(r)[1] for r in range(3)) == 40
+    assert plan.n_rounds == 2 and plan.round_block(1, 1) == (32, 4) and plan.round_block(1, 2)[1] == 0
     g = Geometry.from_spec(SPEC)
-    ex = [plan_exchange(g, plan, r) for r in range(3)]
-    for r in range(3):
-        for h in range(3):
-            assert ex[r].send[h] == ex[h].recv[r]  # what r sends to h is what h expects from r
+    for t in range(plan.n_rounds):
+        ex = [plan_exchange(g, plan, r, t) for r in range(3)]
+        for r in range(3):
+            for h in range(3):
+                # what r sends to h is what h expects from r
+                assert ex[r].send[h] == ex[h].recv[r]
+                assert ex[r].send_sizes[h] == ex[h].recv_sizes[r]
 
 
 def test_band_exchange_volume_config4_p8():
@@ -122,7 +143,9 @@ def test_band_exchange_volume_config4_p8():
     spec = synth.config(4)
     g = Geometry.from_spec(spec)
     plan = SlabPlan(8, spec.Nz, spec.Np)
-    ex = plan_exchange(g, plan, 0)
-    rows = sum(plan.views(r)[1] * (hi - lo + 1) for r, (lo, hi) in enumerate(ex.recv))
+    rows = 0
+    for t in range(plan.n_rounds):
+        ex = plan_exchange(g, plan, 0, t)
+        rows += sum(ex.views[r][1] * (hi - lo + 1) for r, (lo, hi) in enumerate(ex.recv))
     full = spec.Np * spec.Nv
     assert rows / full < 0.2, rows / full

@@ -283,32 +283,48 @@ def test_synth_gpu_generator_matches_cpu(torch_cuda):
 
 
 def test_kslab_driver_single_rank_equals_reconstruct(torch_cuda):
-    """dist.kslab_reconstruct at world size 1 (filter, band slicing, per-source BP) and the
-    per-rank computation for world sizes 2 and 4 (each rank's slab from the bands it would
-    receive) are bitwise equal to ifdk_reconstruct."""
+    """dist.kslab_reconstruct at world size 1 (pipelined rounds of 128-view blocks on three
+    streams), its end-to-end host form, and the per-rank computation for world sizes 2 and 4
+    (each rank's slab from the bands it would receive, round by round) are bitwise equal to
+    ifdk_reconstruct."""
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_backproject, ifdk_filter, ifdk_reconstruct
-    from paper_1909_02724_b200.dist import SlabPlan, kslab_reconstruct, plan_exchange
+    from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct, kslab_reconstruct_host,
+                                            plan_exchange)
 
-    spec = _spec(512, 128, 128, 96, 96, 256)
+    spec = _spec(600, 128, 128, 96, 96, 320)  # 5 blocks: a short last block
     g = Geometry.from_spec(spec)
     raw = torch.from_numpy(_phantom_E(spec)).cuda()
     ref = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
     ifdk_reconstruct(g, raw, ref)
+    plan1 = SlabPlan(1, spec.Nz, spec.Np)
     vol = torch.empty_like(ref)
-    kslab_reconstruct(g, raw, vol, SlabPlan(1, spec.Nz, spec.Np), 0)
+    timings = {}
+    kslab_reconstruct(g, raw, vol, plan1, 0, timings=timings)
     assert torch.equal(vol, ref)
+    assert timings["rounds"] == 5 and timings["bp_ms"] > 0
+    raw_h = raw.cpu().pin_memory()
+    vol_h = torch.full(ref.shape, float("nan")).pin_memory()
+    vol2 = torch.empty_like(ref)
+    kslab_reconstruct_host(g, raw_h, vol2, vol_h, plan1, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(vol_h, ref.cpu())
     Q = torch.empty_like(raw)
     ifdk_filter(g, raw, Q)
     for world in (2, 4):
         plan = SlabPlan(world, spec.Nz, spec.Np)
         for rank in range(world):
             k0, nk = plan.slab(rank)
-            ex = plan_exchange(g, plan, rank)
             slab = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
-            for r in range(world):  # the bands rank r would send to this rank, in view order
-                s0, n = plan.views(r)
-                lo, hi = ex.recv[r]
-                ifdk_backproject(g, Q[s0:s0 + n, lo:hi + 1].contiguous(), s0, slab, k0=k0, v0=lo,
-                                 accumulate=r > 0)
+            first = True
+            for t in range(plan.n_rounds):
+                ex = plan_exchange(g, plan, rank, t)
+                for r in range(world):  # the bands rank r sends this rank in round t
+                    s0, n = ex.views[r]
+                    lo, hi = ex.recv[r]
+                    if n == 0 or hi < lo:
+                        continue
+                    ifdk_backproject(g, Q[s0:s0 + n, lo:hi + 1].contiguous(), s0, slab, k0=k0,
+                                     v0=lo, accumulate=not first)
+                    first = False
             assert torch.equal(slab, ref[k0:k0 + nk]), (world, rank)
