@@ -8,6 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libifdk.so")
+PROBE_LIB = os.path.join(HERE, "libifdk_probe.so")  # shared-memory roofline micro-benchmark
 SOURCES = ["geometry.cpp", "filter.cu", "backproject.cu", "api.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
@@ -25,7 +26,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def build_probe(force: bool = False) -> str:
+    src = os.path.join(CSRC, "probe.cu")
+    if force or not os.path.exists(PROBE_LIB) or os.path.getmtime(src) > os.path.getmtime(PROBE_LIB):
+        cmd = ["nvcc", *NVCC_FLAGS, "-shared", src, "-o", PROBE_LIB + ".tmp", "-lcudart"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building libifdk_probe.so")
+        os.replace(PROBE_LIB + ".tmp", PROBE_LIB)
+    return PROBE_LIB
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_probe(force)
     if not force and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, s) for s in SOURCES]

@@ -64,7 +64,8 @@ struct BPParams {
     int raw_bytes;    // bytes of one raw box (multiple of 128)
     int vb;           // view batch of the two-level summation
     uint32_t neg_magic;  // -0x4B000000 * P2 * 8 mod 2^32 (see accumulate_view_smem)
-    int pair;            // PAIR walk (dv < 1 everywhere)
+    int pair;            // rows of slack for a multi-slice walk (PAIR / TRIPLE): 1, else 0
+    int walk;            // slices per floor: 1, 2 (PAIR) or 3 (TRIPLE)
     int accumulate;
 };
 
@@ -185,7 +186,7 @@ __device__ __forceinline__ uint32_t floor_bits(float v, float* fr)
 // `hook(q)` runs once per 8-slice group q (0 .. KC/8 - 1) in program order with the group's
 // updates: the kernel uses it to transform row q of the next view's patch while this view's
 // shared loads are in flight.
-template <int KC, int P2, bool FULL, bool PAIR, typename Hook>
+template <int KC, int P2, bool FULL, int WALK, typename Hook>
 __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t pair_base,
                                                      uint32_t neg_magic, const ThreadInv& t,
                                                      int u_org, int v_org, int kv0, int kv1,
@@ -198,7 +199,53 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
         pair_base + (uint32_t)(((t.nv - v_org) * P2 + (t.nu - u_org)) * 8) + neg_magic;
     constexpr uint32_t S = P2 * 8;
     float fv0 = t.fv0;
-    if constexpr (PAIR) {
+    if constexpr (WALK == 3) {
+        // TRIPLE (needs 0.5 <= dv < 1, configs 1-4): slices kk, kk+1, kk+2 lie within rows
+        // n .. n+3 (fr + 2 dv < 3), and slice kk+2 sits g2 = fr + 2 dv - 2 in [-1, 1) rows past
+        // row n+2 (2 dv >= 1): four LDS.64 and one floor serve three updates, 10.7 B of shared
+        // memory per update.
+#pragma unroll
+        for (int kk = 0; kk + 3 <= KC; kk += 3) {
+            if (kk == 0 || (kk >> 3) != ((kk - 3) >> 3)) {  // first triple of an 8-slice group
+                hook(kk >> 3);
+                asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            }
+            float fr0;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
+            const uint32_t addr = bits * S + a0;
+            const float2 p0 = lds64(addr);
+            const float2 p1 = lds64(addr + S);
+            const float2 p2 = lds64(addr + 2 * S);
+            const float2 p3 = lds64(addr + 3 * S);
+            const float h0 = fmaf(t.du, p0.y, p0.x);  // Alg. alg:subpixel lines 4-5
+            const float h1 = fmaf(t.du, p1.y, p1.x);
+            const float h2 = fmaf(t.du, p2.y, p2.x);
+            const float h3 = fmaf(t.du, p3.y, p3.x);
+            const float d01 = h1 - h0, d12 = h2 - h1;
+            if (FULL || (kk >= kv0 && kk < kv1))
+                acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);  // line 6; Alg. alg:bp line 10
+            const float g1 = fr0 + t.dvm1;
+            const float e1 = g1 >= 0.f ? d12 : d01;
+            if (FULL || (kk + 1 >= kv0 && kk + 1 < kv1))
+                acc[kk + 1] = fmaf(t.W, fmaf(g1, e1, h1), acc[kk + 1]);
+            const float g2 = g1 + t.dvm1;  // fr + 2 dv - 2
+            const float e2 = g2 >= 0.f ? h3 - h2 : d12;
+            if (FULL || (kk + 2 >= kv0 && kk + 2 < kv1))
+                acc[kk + 2] = fmaf(t.W, fmaf(g2, e2, h2), acc[kk + 2]);
+        }
+#pragma unroll
+        for (int kk = KC - KC % 3; kk < KC; ++kk) {  // the chunk's last KC mod 3 slices
+            float fr;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
+            const uint32_t addr = bits * S + a0;
+            const float2 p0 = lds64(addr);
+            const float2 p1 = lds64(addr + S);
+            const float h0 = fmaf(t.du, p0.y, p0.x);
+            const float h1 = fmaf(t.du, p1.y, p1.x);
+            if (FULL || (kk >= kv0 && kk < kv1))
+                acc[kk] = fmaf(t.W, fmaf(fr, h1 - h0, h0), acc[kk]);
+        }
+    } else if constexpr (WALK == 2) {
 #pragma unroll
         for (int kk = 0; kk < KC; kk += 2) {
             // Every 8 slices, launder fv0 through a volatile asm so that the compiler cannot
@@ -322,6 +369,7 @@ __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i
 // 8 warps compute the boxes of the next 8 views together, so no warp straggles at the barrier.
 constexpr int kMetaRing = 16;
 
+template <int KC, int WALK>
 __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, int t, int i_lo,
                               int i_hi, int j_lo, int j_hi, int kb, int kv0, int kv1)
 {
@@ -338,7 +386,14 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
     double umin = c.u, umax = c.u;
     // slices whose rows are read: the PAIR walk reads from the even slice below kv0 to the odd
     // slice at or above kv1 - 1, and one row more (h_need below)
-    const int ka = p.pair ? (kv0 & ~1) : kv0, kz = p.pair ? ((kv1 - 1) | 1) : kv1 - 1;
+    int ka = kv0, kz = kv1 - 1;
+    if constexpr (WALK == 2) {
+        ka = kv0 & ~1;
+        kz = (kv1 - 1) | 1;
+    } else if constexpr (WALK == 3) {  // triples start on multiples of 3; the tail is single
+        ka = kv0 - kv0 % 3;
+        kz = min((kv1 - 1) / 3 * 3 + 2, KC - 1);
+    }
     const double va = c.v + ka * c.dv, vb = c.v + kz * c.dv;
     double vmin = fmin(va, vb), vmax = fmax(va, vb);
 #pragma unroll
@@ -365,7 +420,7 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
     }
 }
 
-template <int KC, int P2, bool TMA, bool PAIR>
+template <int KC, int P2, bool TMA, int WALK>
 __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     bp_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
               const __grid_constant__ PTable pt)
@@ -443,7 +498,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     };
     auto metas = [=](int t0) {  // all warps: boxes of views t0 .. t0+7
         if (t0 + warp < n)
-            compute_meta1(meta, p, ptab->P[t0 + warp], t0 + warp, i_lo, i_hi, j_lo, j_hi, kb, kv0,
+            compute_meta1<KC, WALK>(meta, p, ptab->P[t0 + warp], t0 + warp, i_lo, i_hi, j_lo, j_hi, kb, kv0,
                           kv1);
     };
 
@@ -518,10 +573,10 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
             };
             const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
             if (full)
-                accumulate_view_smem<KC, P2, true, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
+                accumulate_view_smem<KC, P2, true, WALK>(acc, pb, p.neg_magic, ti, u_org, v_org,
                                                          kv0, kv1, row);
             else
-                accumulate_view_smem<KC, P2, false, PAIR>(acc, pb, p.neg_magic, ti, u_org, v_org,
+                accumulate_view_smem<KC, P2, false, WALK>(acc, pb, p.neg_magic, ti, u_org, v_org,
                                                           kv0, kv1, row);
             if (nxt) {
                 if (narrow) {
@@ -531,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
                 }
             }
         } else {
-            accumulate_view_global<KC, PAIR>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0,
+            accumulate_view_global<KC, (WALK >= 2)>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0,
                                              kv1);
         }
         if (t == next_flush || t == n - 1) {
@@ -561,18 +616,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode()
     return fn;
 }
 
-template <int KC, int P2, bool PAIR>
+template <int KC, int P2, int WALK>
 ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, const PTable& pt, bool tma,
                      dim3 grid, size_t smem, cudaStream_t st)
 {
     cudaError_t e;
     if (tma) {
-        auto k = bp_kernel<KC, P2, true, PAIR>;
+        auto k = bp_kernel<KC, P2, true, WALK>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp)");
         k<<<grid, kThreads, smem, st>>>(p, map, pt);
     } else {
-        auto k = bp_kernel<KC, P2, false, PAIR>;
+        auto k = bp_kernel<KC, P2, false, (WALK >= 2 ? 2 : 1)>;
         k<<<grid, kThreads, 0, st>>>(p, map, pt);
     }
     e = cudaGetLastError();
@@ -587,6 +642,23 @@ bool use_pair(const ifdk_geometry* g)
     const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
     const char* pe = std::getenv("IFDK_BP_PAIR");
     return dv_max < 0.999 && !(pe && pe[0] == '0');
+}
+
+// Slices per floor of the k-walk: 2 (PAIR) when dv/dk < 1 for every z (all five configs),
+// else 1.  IFDK_BP_WALK=3 selects the TRIPLE walk where 0.5 <= dv/dk < 1 (configs 1-4): it
+// needs 11 % less shared-memory traffic per update but measured slower on B200 (config 4,
+// 256 views: 1672 GUPS vs 1800 for PAIR), so it is an opt-in variant.  (IFDK_BP_PAIR=0 forces
+// one floor per slice, with 32-slice chunks.)
+int choose_walk(const ifdk_geometry* g)
+{
+    if (!use_pair(g)) return 1;
+    int w = 2;
+    if (const char* e = std::getenv("IFDK_BP_WALK")) {
+        const int v = std::atoi(e);
+        const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
+        if (v == 3 && dv_min >= 0.5001) w = 3;
+    }
+    return w;
 }
 
 // Slices per k-chunk (= register accumulators per thread).  The choice depends on the geometry
@@ -645,6 +717,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
     p.pair = use_pair(g) ? 1 : 0;
+    p.walk = KC == 64 ? choose_walk(g) : (p.pair ? 2 : 1);
     int box_h = (int)std::ceil(hb) + 6 + p.pair;
     if (box_w < 8) box_w = 8;
     int P2 = 0;
@@ -678,26 +751,33 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
     dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
     ifdk_status s;
-    if (p.pair && KC == 64) {
+    if (p.walk == 3) {
         switch (P2) {
-            case 24: s = launch_t<64, 24, true>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<64, 40, true>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<64, 56, true>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<64, 72, true>(p, map, pt, tma, grid, smem, st); break;
+            case 24: s = launch_t<64, 24, 3>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<64, 40, 3>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<64, 56, 3>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<64, 72, 3>(p, map, pt, tma, grid, smem, st); break;
         }
-    } else if (p.pair) {
+    } else if (p.walk == 2 && KC == 64) {
         switch (P2) {
-            case 24: s = launch_t<32, 24, true>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40, true>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56, true>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72, true>(p, map, pt, tma, grid, smem, st); break;
+            case 24: s = launch_t<64, 24, 2>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<64, 40, 2>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<64, 56, 2>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<64, 72, 2>(p, map, pt, tma, grid, smem, st); break;
+        }
+    } else if (p.walk == 2) {
+        switch (P2) {
+            case 24: s = launch_t<32, 24, 2>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40, 2>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56, 2>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72, 2>(p, map, pt, tma, grid, smem, st); break;
         }
     } else {
         switch (P2) {
-            case 24: s = launch_t<32, 24, false>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40, false>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56, false>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72, false>(p, map, pt, tma, grid, smem, st); break;
+            case 24: s = launch_t<32, 24, 1>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<32, 40, 1>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<32, 56, 1>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<32, 72, 1>(p, map, pt, tma, grid, smem, st); break;
         }
     }
     return s;
