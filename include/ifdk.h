@@ -119,6 +119,21 @@ ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw_dev, long 
 ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float* raw_host, long n_views,
                                   float* vol_host, void* stream);
 
+/* MEASURED BASELINE, not the production path: the paper's
+ * straightforward kernel -- Alg. alg:bp per voxel with fp32
+ * coordinates [x,y,z] = P_s [i,j,k,1] -- with the bilinear sample of Alg.
+ * alg:subpixel taken by the texture unit (texture = 1: cudaFilterModeLinear,
+ * 8-bit fixed-point weights, border mode = per-tap zero border) or in software
+ * from global memory (texture = 0).  filtered_dev holds all Nv rows of each view
+ * ([n_views][Nv][Nu]); vol_dev is the slab k0..k0+nk-1 ([nk][Ny][Nx]),
+ * overwritten (accumulate = 0) or added to (1).  Its error against the fp64
+ * oracle exceeds the tolerance ifdk_backproject meets.
+ * texture = 1 allocates a layered CUDA array per 256 views and synchronises
+ * `stream` before returning.  Errors as ifdk_backproject. */
+ifdk_status ifdk_backproject_alg2(const ifdk_geometry* g, const float* filtered_dev, long s0,
+                                  long n_views, float* vol_dev, int k0, int nk, int accumulate,
+                                  int texture, void* stream);
+
 /* Number of device kernels the last successful call on this thread launched. */
 int ifdk_last_launch_count(void);
 

@@ -9,6 +9,7 @@ from .ifdk import (  # noqa: F401
     Geometry,
     IfdkError,
     ifdk_backproject,
+    ifdk_backproject_alg2,
     ifdk_filter,
     ifdk_reconstruct,
     ifdk_reconstruct_host,

@@ -62,4 +62,9 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
                                cudaStream_t st);
 
+// baseline.cu (measured baselines, not the production path)
+ifdk_status launch_backproject_alg2(const ifdk_geometry* g, const float* Q, long s0, long n_views,
+                                    float* vol, int k0, int nk, int accumulate, int hw,
+                                    cudaStream_t st);
+
 }  // namespace ifdk

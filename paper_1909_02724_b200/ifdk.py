@@ -35,6 +35,7 @@ EXPORTS = (
     "ifdk_band_rows",
     "ifdk_filter",
     "ifdk_backproject",
+    "ifdk_backproject_alg2",
     "ifdk_reconstruct",
     "ifdk_reconstruct_host",
     "ifdk_last_launch_count",
@@ -67,6 +68,8 @@ _lib.ifdk_filter.argtypes = [_vp, _vp, _vp, _l, _i, _i, _vp]
 _lib.ifdk_filter.restype = _i
 _lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp]
 _lib.ifdk_backproject.restype = _i
+_lib.ifdk_backproject_alg2.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _i, _i, _vp]
+_lib.ifdk_backproject_alg2.restype = _i
 _lib.ifdk_reconstruct.argtypes = [_vp, _vp, _l, _vp, _vp]
 _lib.ifdk_reconstruct.restype = _i
 _lib.ifdk_reconstruct_host.argtypes = [_vp, _vp, _l, _vp, _vp]
@@ -169,6 +172,20 @@ def ifdk_backproject(g: Geometry, filtered, s0: int, vol, k0: int = 0, v0: int =
                                  filtered.shape[0], int(v0), filtered.shape[1],
                                  _dev_f32(vol, "vol"), int(k0), vol.shape[0],
                                  1 if accumulate else 0, _stream_ptr(stream)))
+
+
+def ifdk_backproject_alg2(g: Geometry, filtered, s0: int, vol, k0: int = 0,
+                          accumulate: bool = False, texture: bool = True, stream=None) -> None:
+    """MEASURED BASELINE (not the production path): the paper's per-voxel fp32 Alg. alg:bp with
+    hardware-texture (texture=True) or software bilinear sampling; filtered [n][Nv][Nu]."""
+    if filtered.dim() != 3 or filtered.shape[1] != g.Nv or filtered.shape[2] != g.Nu:
+        raise ValueError("filtered must be [n_views][Nv][Nu]")
+    if vol.dim() != 3 or vol.shape[1] != g.Ny or vol.shape[2] != g.Nx:
+        raise ValueError("vol must be [nk][Ny][Nx]")
+    _check(_lib.ifdk_backproject_alg2(g.handle, _dev_f32(filtered, "filtered"), int(s0),
+                                      filtered.shape[0], _dev_f32(vol, "vol"), int(k0),
+                                      vol.shape[0], 1 if accumulate else 0, 1 if texture else 0,
+                                      _stream_ptr(stream)))
 
 
 def ifdk_reconstruct(g: Geometry, raw, vol, stream=None) -> None:
