@@ -235,7 +235,8 @@ def run_ours(args, spec, rank, world, local_rank):
     import synth
     from paper_1909_02724_b200 import (Geometry, ifdk_backproject, ifdk_filter,
                                        ifdk_reconstruct_host, last_launch_count)
-    from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct, kslab_reconstruct_host,
+    from paper_1909_02724_b200.dist import (GridPlan, SlabPlan, grid_groups, hybrid_reconstruct,
+                                            kslab_reconstruct, kslab_reconstruct_host,
                                             projection_split_reconstruct)
 
     torch.cuda.set_device(local_rank)
@@ -395,32 +396,78 @@ def run_ours(args, spec, rank, world, local_rank):
                "steps": n_e2e, "api": api}
         del raw_h, vol_h
 
-    # The projection-split variant, measured against the slab split in the same run.
+    # The projection-split and R x C grid variants, measured against the slab split in the
+    # same run (a failure is reported in the line instead of losing it).
     variants = {}
-    if world > 1 and not args.no_variants and spec.Nz % world == 0:
-        torch.cuda.empty_cache()
-        need = 4 * (spec.Nz * spec.Ny * spec.Nx + n_local * spec.Nv * spec.Nu)
-        free = torch.cuda.mem_get_info(dev)[0]
-        ok = _max_over_ranks(0.0 if free > 1.05 * need else 1.0, world, dev) == 0.0
-        if ok:
-            ps = torch.empty((spec.Nz // world, spec.Ny, spec.Nx), device=dev)
-            projection_split_reconstruct(g, raw, blocks, ps, world)  # warm-up
-            tm = {}
-            torch.cuda.synchronize()
-            dist.barrier()
-            projection_split_reconstruct(g, raw, blocks, ps, world, timings=tm)
-            pms = _max_over_ranks(tm["wall_ms"], world, dev)
-            same = (k0, nk) == (rank * spec.Nz // world, spec.Nz // world)
-            dmax = float((ps - vol).abs().max()) if same else float("nan")
-            vmax = _max_over_ranks(float(vol.abs().max()), world, dev)
-            variants["projection_split"] = {
-                "value": gups(spec, pms / 1e3), "unit": "GUPS", "ms_per_step": pms,
-                "reduce_scatter_ms": _max_over_ranks(tm["reduce_scatter_ms"], world, dev),
-                "max_abs_diff_vs_kslab_rel": _max_over_ranks(dmax, world, dev) / vmax}
-            del ps
-        else:
-            variants["projection_split"] = {"skipped": "full partial volume does not fit"}
 
+    def measure_variants():
+        nonlocal raw
+        if world > 1 and not args.no_variants and spec.Nz % world == 0:
+            torch.cuda.empty_cache()
+            need = 4 * (spec.Nz * spec.Ny * spec.Nx + n_local * spec.Nv * spec.Nu)
+            free = torch.cuda.mem_get_info(dev)[0]
+            ok = _max_over_ranks(0.0 if free > 1.05 * need else 1.0, world, dev) == 0.0
+            if ok:
+                ps = torch.empty((spec.Nz // world, spec.Ny, spec.Nx), device=dev)
+                projection_split_reconstruct(g, raw, blocks, ps, world)  # warm-up
+                tm = {}
+                torch.cuda.synchronize()
+                dist.barrier()
+                projection_split_reconstruct(g, raw, blocks, ps, world, timings=tm)
+                pms = _max_over_ranks(tm["wall_ms"], world, dev)
+                same = (k0, nk) == (rank * spec.Nz // world, spec.Nz // world)
+                dmax = float((ps - vol).abs().max()) if same else float("nan")
+                vmax = _max_over_ranks(float(vol.abs().max()), world, dev)
+                variants["projection_split"] = {
+                    "value": gups(spec, pms / 1e3), "unit": "GUPS", "ms_per_step": pms,
+                    "reduce_scatter_ms": _max_over_ranks(tm["reduce_scatter_ms"], world, dev),
+                    "max_abs_diff_vs_kslab_rel": _max_over_ranks(dmax, world, dev) / vmax}
+                del ps
+            else:
+                variants["projection_split"] = {"skipped": "full partial volume does not fit"}
+            if world >= 4 and world % 2 == 0:
+                # the paper's R x C grid with C = 2 view columns (band exchange inside a column,
+                # reduce-scatter across a row); its own view blocks are generated for it
+                R, C = world // 2, 2
+                grid = GridPlan(R, C, spec.Nz, spec.Np)
+                rows, cols = grid_groups(grid)
+                gr, gc = grid.coords(rank)
+                gblocks = grid.column_plan(gc).local_views(gr)
+                del raw
+                torch.cuda.empty_cache()
+                graw = torch.empty((sum(n for _, n in gblocks), spec.Nv, spec.Nu), device=dev)
+                off = 0
+                for s0, n in gblocks:
+                    synth.project_gpu(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta,
+                                      ell, s0, n, 0, spec.Nv, graw[off:off + n].data_ptr(),
+                                      torch.cuda.current_stream().cuda_stream)
+                    off += n
+                sk0, sn = grid.sub_slab(rank)
+                gvol = torch.empty((max(sn, 1), spec.Ny, spec.Nx), device=dev)
+                hybrid_reconstruct(g, graw, gvol[:sn], grid, rank, rows[gr], cols[gc])  # warm-up
+                torch.cuda.synchronize()
+                dist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                hybrid_reconstruct(g, graw, gvol[:sn], grid, rank, rows[gr], cols[gc])
+                e1.record()
+                e1.synchronize()
+                hms = _max_over_ranks(e0.elapsed_time(e1), world, dev)
+                # cross-check against the k-slab result where the two partitions overlap
+                a, b = max(sk0, k0), min(sk0 + sn, k0 + nk)
+                dmax = float((gvol[a - sk0:b - sk0] - vol[a - k0:b - k0]).abs().max()) if b > a else 0.0
+                vmax = _max_over_ranks(float(vol.abs().max()), world, dev)
+                variants[f"grid_{R}x{C}"] = {
+                    "value": gups(spec, hms / 1e3), "unit": "GUPS", "ms_per_step": hms,
+                    "max_abs_diff_vs_kslab_rel": _max_over_ranks(dmax, world, dev) / vmax}
+                del graw, gvol
+
+
+    if world > 1 and not args.no_variants:
+        try:
+            measure_variants()
+        except Exception as exc:  # noqa: BLE001
+            variants["error"] = repr(exc)[:300]
     if rank != 0:
         return
     cpu = None

@@ -53,12 +53,17 @@ def _split(n: int, parts: int, quantum: int) -> list[int]:
 
 @dataclass(frozen=True)
 class SlabPlan:
-    """Which slab rank r owns, and which view blocks (k-slab split)."""
+    """Which slab rank r owns, and which view blocks (k-slab split).
+
+    The plan covers the global view blocks offset, offset + stride, offset + 2 stride, ...
+    (all blocks by default; one column of an R x C grid otherwise, see hybrid_reconstruct)."""
 
     world: int
     Nz: int
     Np: int
     block: int = VIEW_BATCH
+    stride: int = 1
+    offset: int = 0
 
     @property
     def k_bounds(self) -> list[int]:
@@ -70,15 +75,18 @@ class SlabPlan:
 
     @property
     def n_blocks(self) -> int:
-        return (self.Np + self.block - 1) // self.block
+        total = (self.Np + self.block - 1) // self.block
+        return max(0, (total - self.offset + self.stride - 1) // self.stride)
 
     @property
     def n_rounds(self) -> int:
         return (self.n_blocks + self.world - 1) // self.world
 
     def block_views(self, b: int) -> tuple[int, int]:
-        """(first global view, count) of block b (count 0 past the end)."""
-        s0 = b * self.block
+        """(first global view, count) of the plan's block b (count 0 past the end)."""
+        if b >= self.n_blocks:
+            return self.Np, 0
+        s0 = (self.offset + b * self.stride) * self.block
         return s0, max(0, min(self.block, self.Np - s0))
 
     def round_block(self, t: int, r: int) -> tuple[int, int]:
@@ -386,6 +394,78 @@ def kslab_reconstruct_host(g, raw_host, vol_slab, vol_host, plan: SlabPlan, rank
     streamed to vol_host (pinned) in sub-slabs during the last round."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
                      raw_host=raw_host, vol_host=vol_host, force_exchange=force_exchange)
+
+
+# ----------------------------------------------------------------------------- R x C grid
+@dataclass(frozen=True)
+class GridPlan:
+    """The paper's R x C rank grid: rank = r C + c.  Row r owns volume slab r of R
+    (multiples of the 64-slice chunk); column c owns the view blocks b = c (mod C).  Inside a
+    column the k-slab pipeline runs over its R ranks (band all-to-all); across a row the C
+    partial slabs are summed by a reduce-scatter, leaving rank (r, c) the c-th of C equal
+    sub-slabs of slab r.  R = P, C = 1 is the k-slab split; R = 1, C = P the projection split."""
+
+    R: int
+    C: int
+    Nz: int
+    Np: int
+    block: int = VIEW_BATCH
+
+    def coords(self, rank: int) -> tuple[int, int]:
+        return rank // self.C, rank % self.C
+
+    def column_plan(self, c: int) -> SlabPlan:
+        return SlabPlan(self.R, self.Nz, self.Np, self.block, stride=self.C, offset=c)
+
+    def slab(self, r: int) -> tuple[int, int]:
+        return SlabPlan(self.R, self.Nz, self.Np).slab(r)
+
+    def sub_slab(self, rank: int) -> tuple[int, int]:
+        """Slices (k0, n) rank owns at the end: sub-slab c of slab r, ceil(nk / C) slices
+        each (the last ones may be shorter or empty)."""
+        r, c = self.coords(rank)
+        k0, nk = self.slab(r)
+        q = -(-nk // self.C)
+        a = min(c * q, nk)
+        return k0 + a, min(q, nk - a)
+
+
+def grid_groups(grid: GridPlan):
+    """Row and column process groups of the grid (every rank must call this, in order).
+    Returns (rows, cols): rows[r] spans ranks rC .. rC+C-1, cols[c] ranks c, c+C, ..."""
+    import torch.distributed as dist
+
+    rows = [dist.new_group([r * grid.C + c for c in range(grid.C)]) for r in range(grid.R)]
+    cols = [dist.new_group([r * grid.C + c for r in range(grid.R)]) for c in range(grid.C)]
+    return rows, cols
+
+
+def hybrid_reconstruct(g, raw_local, vol_sub, grid: GridPlan, rank: int, row_group, col_group,
+                       filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
+                       timings: Optional[dict] = None):
+    """R x C FDK on one rank.  raw_local: the rank's blocks of its column
+    (grid.column_plan(c).local_views(r)) in order; vol_sub: [n][Ny][Nx] for
+    grid.sub_slab(rank), overwritten.  Equal to one GPU up to fp32 summation order (the C
+    column partial sums are added by the reduce-scatter)."""
+    import torch
+    import torch.distributed as dist
+
+    r, c = grid.coords(rank)
+    plan = grid.column_plan(c)
+    k0, nk = grid.slab(r)
+    q = -(-nk // grid.C)
+    partial = raw_local.new_empty((q * grid.C, g.Ny, g.Nx))
+    partial[nk:].zero_()  # padding rows of the reduce-scatter
+    _pipeline(g, plan, r, partial[:nk], col_group, filter_fn, bp_fn, timings,
+              raw_local=raw_local)
+    sk0, sn = grid.sub_slab(rank)
+    if grid.C > 1:
+        out = raw_local.new_empty((q, g.Ny, g.Nx))
+        dist.reduce_scatter_tensor(out, partial, op=dist.ReduceOp.SUM, group=row_group)
+        vol_sub.copy_(out[:sn])
+    else:
+        vol_sub.copy_(partial[:sn])
+    return vol_sub
 
 
 def projection_split_reconstruct(g, raw_local, blocks, vol_slab, world: int, group=None,
