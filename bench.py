@@ -264,6 +264,7 @@ def run_ours(args, spec, rank, world, local_rank):
         if not use_kslab else None
 
     bp_events = []
+    filter_events = []
 
     def step_single(record):
         """One GPU: per 256-view batch, ifdk_filter then ifdk_backproject (what
@@ -272,16 +273,19 @@ def run_ours(args, spec, rank, world, local_rank):
         for b0 in range(0, n_local, batch):
             nb = min(batch, n_local - b0)
             q = Q[:nb]
+            if record:
+                f0, e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+                f0.record()
             ifdk_filter(g, raw[b0:b0 + nb], q)
             launches += last_launch_count()
             if record:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
             ifdk_backproject(g, q, b0, vol, accumulate=b0 > 0)
             launches += last_launch_count()
             if record:
                 e1.record()
                 bp_events.append((e0, e1, nb))
+                filter_events.append((f0, e0, nb))
         return launches
 
     timings = {}
@@ -344,6 +348,26 @@ def run_ours(args, spec, rank, world, local_rank):
         upd_per_launch = spec.Nx * spec.Ny * nk * spec.Np / max(plan.n_rounds, 1)
         bp_share = stage.get("bp_ms", float("nan")) / ms
     achieved_gbs = SMEM_BYTES_PER_UPDATE * upd_per_launch / bp_s / 1e9
+    hbm_peak = float(measured_peaks().get("hbm_gbs", 6543.4))
+    # BP against HBM: algorithmic bytes of one launch = its filtered views read once + the
+    # slab written (first launch) or read and written (accumulating launches): 8 B per voxel
+    # per launch in the steady state.
+    views_per_launch = upd_per_launch / (spec.Nx * spec.Ny * nk)
+    bp_hbm_bytes = 4 * views_per_launch * spec.Nu * spec.Nv + 8 * spec.Nx * spec.Ny * nk
+    roofline_hbm = {"bound": "hbm", "achieved": bp_hbm_bytes / bp_s / 1e9, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": bp_hbm_bytes / bp_s / 1e9 / hbm_peak,
+                    "kernel": "bp_kernel (4 B per filtered pixel + 8 B per voxel per launch)",
+                    "peak_basis": "MEASURED_PEAKS.json hbm_gbs"}
+    filt = None
+    if filter_events:
+        fdur = sum(a.elapsed_time(b) for a, b, _ in filter_events) / len(filter_events) / 1e3
+        fpix = sum(nb for _, _, nb in filter_events) / len(filter_events) * spec.Nu * spec.Nv
+        filt = {"kernel": "filter_f4k_kernel (cosine weight + ramp FFT filter)",
+                "ms_per_launch": fdur * 1e3, "bound": "hbm",
+                "achieved": 8 * fpix / fdur / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": 8 * fpix / fdur / 1e9 / hbm_peak,
+                "note": "8 algorithmic B/pixel (read E, write Q); the kernel is FP32-issue "
+                        "bound by the FFT's instructions (DESIGN.md section 7)"}
     derived_gbs = N_SM * SMEM_B_PER_CLK_PER_SM * 1965e6 / 1e9  # guide: 128 B/clk/SM at max clock
     if smem_bw:
         peak_gbs = smem_bw / 1e9
@@ -509,6 +533,8 @@ def run_ours(args, spec, rank, world, local_rank):
                      "traffic": ncu_traffic(args.config),
                      "kernel": "bp_kernel (16 algorithmic B/update of bilinear taps)",
                      "peak_basis": peak_basis},
+        "roofline_hbm": roofline_hbm,
+        "filter_roofline": filt,
         "clocks": clk,
         "e2e": e2e,
         "gpu_launches": launches,

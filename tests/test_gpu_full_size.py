@@ -61,7 +61,7 @@ def _gen_raw(torch, spec, s0, n):
     return raw
 
 
-@pytest.mark.parametrize("cfg", [3, 4])
+@pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_full_config_sampled_parity(torch_cuda, cfg):
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_reconstruct
