@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip timing configs 1-3 at N = 1")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the projection-split measurement at N > 1")
     ap.add_argument("--path", default="auto", choices=["auto", "kslab"],
@@ -492,6 +494,37 @@ def run_ours(args, spec, rank, world, local_rank):
             measure_variants()
         except Exception as exc:  # noqa: BLE001
             variants["error"] = repr(exc)[:300]
+    # The smaller configs on the same GPU (device-resident raw views, ifdk_reconstruct, median
+    # of 3 after a warm-up): config 1 is latency-bound (no roofline claim), 2 and 3 full size.
+    others = {}
+    if world == 1 and not args.no_other_configs:
+        from paper_1909_02724_b200 import ifdk_reconstruct
+
+        for oc in (1, 2, 3):
+            if oc == args.config:
+                continue
+            os_ = synth.config(oc)
+            og_ = Geometry.from_spec(os_)
+            oraw = torch.empty((os_.Np, os_.Nv, os_.Nu), device=dev)
+            synth.project_gpu(os_.Nu, os_.Nv, os_.Du, os_.Dv, os_.D, os_.d, os_.theta,
+                              synth.default_ellipsoids(os_), 0, os_.Np, 0, os_.Nv,
+                              oraw.data_ptr(), stream.cuda_stream)
+            ovol = torch.empty((os_.Nz, os_.Ny, os_.Nx), device=dev)
+            ifdk_reconstruct(og_, oraw, ovol)
+            ts = []
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                ifdk_reconstruct(og_, oraw, ovol)
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            t_ms = sorted(ts)[1]
+            others[os_.name] = {"fdk_ms": t_ms, "gups": gups(os_, t_ms / 1e3),
+                                "kernel_launches": last_launch_count()}
+            del oraw, ovol
+        torch.cuda.empty_cache()
+
     if rank != 0:
         return
     cpu = None
@@ -544,6 +577,8 @@ def run_ours(args, spec, rank, world, local_rank):
         out["stage_ms"] = stage
     if variants:
         out["variants"] = variants
+    if others:
+        out["other_configs"] = others
     print(json.dumps(out), flush=True)
 
 
