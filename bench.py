@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl"],
+                    help="k-slab band exchange: fused filter + NVLink scatter (auto) or NCCL")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip timing configs 1-3 at N = 1")
     ap.add_argument("--no-variants", action="store_true",
@@ -304,7 +306,8 @@ def run_ours(args, spec, rank, world, local_rank):
     def step_multi(record):
         counter[0] = 0
         kslab_reconstruct(g, raw, vol, plan, rank, filter_fn=f_fn, bp_fn=b_fn,
-                          timings=timings if record else None, force_exchange=True)
+                          timings=timings if record else None, force_exchange=True,
+                          exchange=args.exchange)
         return counter[0]
 
     step = step_multi if use_kslab else step_single
@@ -405,13 +408,15 @@ def run_ours(args, spec, rank, world, local_rank):
             e2e_s = (time.perf_counter() - t0) / n_e2e
             api = "ifdk_reconstruct_host (C ABI)"
         else:
-            kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True)
+            kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True,
+                                   exchange=args.exchange)
             torch.cuda.synchronize()
             if world > 1:
                 dist.barrier()
             t0 = time.perf_counter()
             for _ in range(n_e2e):
-                kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True)
+                kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True,
+                                   exchange=args.exchange)
             torch.cuda.synchronize()
             e2e_s = _max_over_ranks((time.perf_counter() - t0) / n_e2e, world, dev)
             api = "dist.kslab_reconstruct_host (per rank: H2D of its blocks, D2H of its slab)"

@@ -88,6 +88,27 @@ ifdk_status ifdk_band_rows(const ifdk_geometry* g, int k0, int nk, long s, int* 
 ifdk_status ifdk_filter(const ifdk_geometry* g, const float* raw_dev, float* filtered_dev,
                         long n_views, int v0, int n_rows, void* stream);
 
+/* One destination of ifdk_filter_scatter: rows v_lo..v_hi (inclusive) of every
+ * filtered view t are written to base[(t (v_hi - v_lo + 1) + v - v_lo) Nu + u].
+ * base is a device pointer on the current device or a peer device's memory mapped
+ * into this one (CUDA IPC / symmetric memory over NVLink); caller-owned. */
+typedef struct {
+    float* base;
+    int v_lo, v_hi;
+} ifdk_band_dest;
+
+/* Alg. alg:filter exactly as ifdk_filter (bitwise the same values), fused with the
+ * row-band exchange of the k-slab split: instead of one output array,
+ * each filtered row is stored straight into every destination band that contains
+ * it (n_dest <= 16; dests is a host array, copied at launch).  With peer-mapped
+ * bases the NVLink transfer of a row overlaps the filtering of the next ones; the
+ * caller orders the destinations' later reads (e.g. a cross-GPU barrier).
+ * Errors: INVALID_ARGUMENT (NULL pointers, n_dest < 1 or > 16, a band outside
+ * [0, Nv) or empty), SHAPE (rows outside [0, Nv), n_views < 0). */
+ifdk_status ifdk_filter_scatter(const ifdk_geometry* g, const float* raw_dev, long n_views,
+                                int v0, int n_rows, int n_dest, const ifdk_band_dest* dests,
+                                void* stream);
+
 /* Alg. alg:bp + alg:subpixel for views s0..s0+n_views-1 into the
  * slab k0..k0+nk-1:  vol_dev[k-k0][j][i] (=|+=) sum_s f^2 . interp2(Q_s, u, v).
  * filtered_dev holds detector rows v0..v0+n_rows-1 of each view

@@ -11,6 +11,7 @@ from .ifdk import (  # noqa: F401
     ifdk_backproject,
     ifdk_backproject_alg2,
     ifdk_filter,
+    ifdk_filter_scatter,
     ifdk_reconstruct,
     ifdk_reconstruct_host,
     last_launch_count,

@@ -91,6 +91,25 @@ extern "C" ifdk_status ifdk_filter(const ifdk_geometry* g, const float* raw_dev,
                          n_rows, (cudaStream_t)stream);
 }
 
+extern "C" ifdk_status ifdk_filter_scatter(const ifdk_geometry* g, const float* raw_dev,
+                                           long n_views, int v0, int n_rows, int n_dest,
+                                           const ifdk_band_dest* dests, void* stream)
+{
+    t_launches = 0;
+    if (!g || !raw_dev || !dests) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_dest < 1 || n_dest > kMaxFilterDest)
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "n_dest must be 1..16");
+    for (int d = 0; d < n_dest; ++d)
+        if (!dests[d].base || dests[d].v_lo < 0 || dests[d].v_hi >= g->Nv ||
+            dests[d].v_hi < dests[d].v_lo)
+            return fail(IFDK_ERR_INVALID_ARGUMENT, "destination band NULL, empty or outside [0, Nv)");
+    ifdk_status s = check_band(g, n_views, v0, n_rows);
+    if (s != IFDK_OK) return s;
+    if ((s = need_device()) != IFDK_OK) return s;
+    return launch_filter(const_cast<ifdk_geometry*>(g), raw_dev, nullptr, n_views, v0, n_rows,
+                         (cudaStream_t)stream, n_dest, dests);
+}
+
 extern "C" ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* filtered_dev,
                                         long s0, long n_views, int v0, int n_rows, float* vol_dev,
                                         int k0, int nk, int accumulate, void* stream)

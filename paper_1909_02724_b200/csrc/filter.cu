@@ -25,13 +25,28 @@ constexpr int kThreads = 256;
 
 struct FilterParams {
     const float* raw;
-    float* out;
+    float* out;         // [n_views][n_rows][Nu] (n_dest == 0)
     long n_rows_total;  // n_views * n_rows
     int n_rows;         // rows per view
     int v0;             // first detector row of each view
     int Nu;
     float D2, D, Du, Dv, cu, cv;
+    // Band scatter (n_dest > 0): row v of view t goes to every destination d with
+    // lo[d] <= v <= hi[d], at base[d] + (t (hi[d]-lo[d]+1) + v - lo[d]) Nu -- local or
+    // peer-mapped (NVLink) memory, so the exchange of the k-slab split rides the filter.
+    int n_dest;
+    float* base[kMaxFilterDest];
+    int lo[kMaxFilterDest], hi[kMaxFilterDest];
 };
+
+// Output row r (= t n_rows + (v - v0)) of destination d, or nullptr if v is outside its band.
+__device__ __forceinline__ float* dest_row(const FilterParams& p, long r, int d)
+{
+    const long t = r / p.n_rows;
+    const int v = p.v0 + (int)(r - t * p.n_rows);
+    if (v < p.lo[d] || v > p.hi[d]) return nullptr;
+    return p.base[d] + (t * (p.hi[d] - p.lo[d] + 1) + (v - p.lo[d])) * (long)p.Nu;
+}
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b)
 {
@@ -143,12 +158,15 @@ __global__ void __launch_bounds__(kThreads) filter_fft_kernel(const FilterParams
         cur = fft_forward(X, other, tw, log2L);
         float2* Z = (cur ? other : X);
         // Q = conj(Z): real part -> row A, -imag part -> row B (first Nu samples).
-        float* qA = p.out + rA * p.Nu;
-        float* qB = p.out + rB * p.Nu;
-        for (int n = threadIdx.x; n < p.Nu; n += kThreads) {
-            const float2 z = Z[n];
-            qA[n] = z.x;
-            if (hasB) qB[n] = -z.y;
+        const int nd = p.n_dest > 0 ? p.n_dest : 1;
+        for (int d = 0; d < nd; ++d) {
+            float* qA = p.n_dest > 0 ? dest_row(p, rA, d) : p.out + rA * p.Nu;
+            float* qB = !hasB ? nullptr : p.n_dest > 0 ? dest_row(p, rB, d) : p.out + rB * p.Nu;
+            for (int n = threadIdx.x; n < p.Nu; n += kThreads) {
+                const float2 z = Z[n];
+                if (qA) qA[n] = z.x;
+                if (qB) qB[n] = -z.y;
+            }
         }
         __syncthreads();
     }
@@ -343,15 +361,19 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             u[m] = make_float2(u[m].x * h, -u[m].y * h);
         }
         fft4096(u, buf, bufB, twA, twB, i);  // buf's last reader was before bufB's barrier
-        // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1.
-        float* qA = p.out + rA * p.Nu;
-        float* qB = p.out + rB * p.Nu;
+        // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1 (to every destination
+        // band that holds the row when scattering).
+        const int nd = p.n_dest > 0 ? p.n_dest : 1;
+        for (int d = 0; d < nd; ++d) {
+            float* qA = p.n_dest > 0 ? dest_row(p, rA, d) : p.out + rA * p.Nu;
+            float* qB = !hasB ? nullptr : p.n_dest > 0 ? dest_row(p, rB, d) : p.out + rB * p.Nu;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-            const int n = i + m * T;
-            if (n < p.Nu) {
-                qA[n] = u[m].x;
-                if (hasB) qB[n] = -u[m].y;
+            for (int m = 0; m < 8; ++m) {
+                const int n = i + m * T;
+                if (n < p.Nu) {
+                    if (qA) qA[n] = u[m].x;
+                    if (qB) qB[n] = -u[m].y;
+                }
             }
         }
     }
@@ -361,7 +383,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
 }  // namespace
 
 ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
-                          int n_rows, cudaStream_t st)
+                          int n_rows, cudaStream_t st, int n_dest, const ifdk_band_dest* dests)
 {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -417,12 +439,19 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
     p.Dv = (float)g->Dv;
     p.cu = (float)g->cu;
     p.cv = (float)g->cv;
+    p.n_dest = n_dest;
+    for (int d = 0; d < kMaxFilterDest; ++d) {
+        p.base[d] = d < n_dest ? dests[d].base : nullptr;
+        p.lo[d] = d < n_dest ? dests[d].v_lo : 0;
+        p.hi[d] = d < n_dest ? dests[d].v_hi : -1;
+    }
     const long pairs = (total + 1) / 2;
     if (L == 4096) {
         long grid = (long)sms * 2;
         if (grid > pairs) grid = pairs;
         // In-place filtering is safe with the prefetch: a pair's rows are fetched before any
-        // CTA writes them (each pair belongs to one CTA) and never read again.
+        // CTA writes them (each pair belongs to one CTA) and never read again.  (A scatter
+        // destination must not alias the raw views.)
         const bool async = (g->Nu % 4) == 0 && (reinterpret_cast<uintptr_t>(raw) % 16) == 0;
         auto k = async ? filter_f4k_kernel<true> : filter_f4k_kernel<false>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4kSmem);

@@ -53,9 +53,11 @@ void ensure_filter_tables_host(ifdk_geometry* g);
 // ti x tj voxel columns and kc slices can touch, over all views and positions.
 void patch_bound(const ifdk_geometry* g, int ti, int tj, int kc, double* w, double* h);
 
-// filter.cu
+// filter.cu (n_dest > 0: write each row to the destination bands instead of `out`)
+constexpr int kMaxFilterDest = 16;
 ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
-                          int n_rows, cudaStream_t st);
+                          int n_rows, cudaStream_t st, int n_dest = 0,
+                          const ifdk_band_dest* dests = nullptr);
 
 // backproject.cu
 ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,

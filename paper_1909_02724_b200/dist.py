@@ -203,8 +203,49 @@ def _default_fns(g, filter_fn, bp_fn):
     return filter_fn, bp_fn
 
 
+_P2P_CACHE: dict = {}
+
+
+def _p2p_buffers(group, numel, dev):
+    """A float32 symmetric-memory buffer of `numel` elements on every rank of `group` and its
+    handle (peer pointers over NVLink, device-side barrier), or None if unavailable.  Cached:
+    the rendezvous is a collective and the allocation persists across calls."""
+    import torch
+    import torch.distributed as dist
+
+    pg = group or dist.group.WORLD
+    key = (id(pg), numel, str(dev))
+    if key in _P2P_CACHE:
+        return _P2P_CACHE[key]
+    hdl = None
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+
+        if hasattr(symm_mem, "enable_symm_mem_for_group"):
+            symm_mem.enable_symm_mem_for_group(pg.group_name)
+        buf = symm_mem.empty(numel, dtype=torch.float32, device=dev)
+        hdl = symm_mem.rendezvous(buf, pg)
+        hdl._ifdk_keepalive = buf
+    except Exception:  # noqa: BLE001 -- no P2P/symmetric memory: the NCCL exchange is used
+        hdl = None
+    # every rank must take the same path
+    ok = torch.tensor([1 if hdl is not None else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=pg)
+    if int(ok.item()) == 0:
+        hdl = None
+    _P2P_CACHE[key] = hdl
+    return hdl
+
+
+def _ifdk_scatter(g, raw, dests):
+    from .ifdk import ifdk_filter_scatter
+
+    ifdk_filter_scatter(g, raw, dests)
+
+
 def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, timings,
-              raw_local=None, raw_host=None, vol_host=None, force_exchange=False):
+              raw_local=None, raw_host=None, vol_host=None, force_exchange=False,
+              exchange="auto", scatter_fn=None):
     import torch
     import torch.distributed as dist
 
@@ -230,8 +271,24 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
     Qbuf = [torch.empty((B, Nv, Nu), device=dev) for _ in range(min(2, rounds))]
     send_max = max([sum(e.send_sizes) for e in exs] + [1])
     recv_max = max([sum(e.recv_sizes) for e in exs] + [1])
-    sendbuf = [torch.empty(send_max, device=dev) for _ in Qbuf] if xchg else None
-    recvbuf = [torch.empty(recv_max, device=dev) for _ in Qbuf] if xchg else None
+    p2p = _p2p_buffers(group, 2 * recv_max, dev) if (xchg and cuda and exchange != "nccl") \
+        else None
+    if p2p is not None:
+        sym = p2p.get_buffer(p2p.rank, (2 * recv_max,), torch.float32)
+        recvbuf = [sym[:recv_max], sym[recv_max:]]
+        sendbuf = None
+        # element offset of my band inside destination h's receive layout, per round
+        p2p_off = []
+        for t in range(rounds):
+            offs_t = []
+            for h in range(world):
+                exh = exchanges(g, plan, h)[t]
+                offs_t.append(sum(exh.recv_sizes[:rank]))
+            p2p_off.append(offs_t)
+        scatter_fn = scatter_fn or (lambda raw, dests: _ifdk_scatter(g, raw, dests))
+    else:
+        sendbuf = [torch.empty(send_max, device=dev) for _ in Qbuf] if xchg else None
+        recvbuf = [torch.empty(recv_max, device=dev) for _ in Qbuf] if xchg else None
     stage = [torch.empty((B, Nv, Nu), device=dev) for _ in Qbuf] if raw_host is not None else None
 
     cur = torch.cuda.current_stream() if cuda else None
@@ -272,19 +329,33 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
             S.wait(S.F, ev_bp_done[q])
             e0 = S.event(True)
             S.record(e0, S.F)
+            src = None
             if n > 0:
                 if raw_host is not None:
                     S.wait(S.F, ev_h2d[q])
                     src = stage[q][:n]
                 else:
                     src = raw_local[offs[bi]:offs[bi] + n]
-                filter_fn(src, Qbuf[q][:n])
-                bi += 1
-            ev_filt_done[q] = S.event()
-            S.record(ev_filt_done[q], S.F)
             work = None
-            if xchg:
+            if xchg and p2p is not None:
+                # fused: every filtered row goes straight into the receive buffers of the
+                # slabs that need it (NVLink stores into peer memory); the first barrier
+                # guarantees every rank's BP of round t-2 has released buffer q, the second
+                # that every rank's rows have landed (system-scope release / acquire).
+                p2p.barrier(channel=0)
                 if n > 0:
+                    dests = [(p2p.buffer_ptrs[h] + 4 * (q * recv_max + p2p_off[t][h]), lo, hi)
+                             for h, (lo, hi) in enumerate(ex.send) if hi >= lo]
+                    scatter_fn(src, dests)
+                    bi += 1
+                p2p.barrier(channel=0)
+                e1 = S.event(True)
+                S.record(e1, S.F)
+                f_marks.append((e0, e1))
+            elif xchg:
+                if n > 0:
+                    filter_fn(src, Qbuf[q][:n])
+                    bi += 1
                     off = 0
                     for (lo, hi), sz in zip(ex.send, ex.send_sizes):
                         if sz:
@@ -299,9 +370,14 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
                                               ex.recv_sizes, ex.send_sizes, group=group,
                                               async_op=True)
             else:
+                if n > 0:
+                    filter_fn(src, Qbuf[q][:n])
+                    bi += 1
                 e1 = S.event(True)
                 S.record(e1, S.F)
                 f_marks.append((e0, e1))
+            ev_filt_done[q] = S.event()  # stage[q] may be refilled
+            S.record(ev_filt_done[q], S.F)
             ev_ready = S.event()
             S.record(ev_ready, S.F)
         with S.on(S.B):
@@ -370,6 +446,8 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
         tc = sum(a.elapsed_time(b) for a, b in c_marks)
         timings.update({"wall_ms": wall, "filter_pack_ms": tf, "bp_ms": tb, "host_copy_ms": tc,
                         "rounds": rounds,
+                        "exchange": ("p2p-fused" if p2p is not None else "nccl") if xchg
+                        else "none",
                         "exchange_bytes_sent": 4 * sum(sum(e.send_sizes) - e.send_sizes[rank]
                                                        for e in exs) if xchg else 0})
     return vol_slab
@@ -377,23 +455,28 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
 
 def kslab_reconstruct(g, raw_local, vol_slab, plan: SlabPlan, rank: int, group=None,
                       filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
-                      timings: Optional[dict] = None, force_exchange: bool = False):
+                      timings: Optional[dict] = None, force_exchange: bool = False,
+                      exchange: str = "auto"):
     """k-slab FDK on one rank.  raw_local: [plan.n_local(rank)][Nv][Nu], the rank's blocks
     (plan.local_views(rank)) in order, device-resident; vol_slab: [nk][Ny][Nx] (slab
-    plan.slab(rank)), overwritten.  Enqueued on side streams that the current stream joins."""
+    plan.slab(rank)), overwritten.  Enqueued on side streams that the current stream joins.
+    exchange: "auto" fuses the band exchange into the filter over symmetric (NVLink peer)
+    memory when the group supports it (ifdk_filter_scatter + device barriers), else NCCL
+    all-to-all; "nccl" forces the all-to-all."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
-                     raw_local=raw_local, force_exchange=force_exchange)
+                     raw_local=raw_local, force_exchange=force_exchange, exchange=exchange)
 
 
 def kslab_reconstruct_host(g, raw_host, vol_slab, vol_host, plan: SlabPlan, rank: int,
                            group=None, filter_fn: Optional[Callable] = None,
                            bp_fn: Optional[Callable] = None, timings: Optional[dict] = None,
-                           force_exchange: bool = False):
+                           force_exchange: bool = False, exchange: str = "auto"):
     """End-to-end k-slab FDK on one rank: raw_host (pinned, the rank's blocks in order) is
     copied block by block one round ahead; vol_slab (device scratch [nk][Ny][Nx]) is
     streamed to vol_host (pinned) in sub-slabs during the last round."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
-                     raw_host=raw_host, vol_host=vol_host, force_exchange=force_exchange)
+                     raw_host=raw_host, vol_host=vol_host, force_exchange=force_exchange,
+                     exchange=exchange)
 
 
 # ----------------------------------------------------------------------------- R x C grid
@@ -442,7 +525,7 @@ def grid_groups(grid: GridPlan):
 
 def hybrid_reconstruct(g, raw_local, vol_sub, grid: GridPlan, rank: int, row_group, col_group,
                        filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
-                       timings: Optional[dict] = None):
+                       timings: Optional[dict] = None, exchange: str = "auto"):
     """R x C FDK on one rank.  raw_local: the rank's blocks of its column
     (grid.column_plan(c).local_views(r)) in order; vol_sub: [n][Ny][Nx] for
     grid.sub_slab(rank), overwritten.  Equal to one GPU up to fp32 summation order (the C
@@ -457,7 +540,7 @@ def hybrid_reconstruct(g, raw_local, vol_sub, grid: GridPlan, rank: int, row_gro
     partial = raw_local.new_empty((q * grid.C, g.Ny, g.Nx))
     partial[nk:].zero_()  # padding rows of the reduce-scatter
     _pipeline(g, plan, r, partial[:nk], col_group, filter_fn, bp_fn, timings,
-              raw_local=raw_local)
+              raw_local=raw_local, exchange=exchange)
     sk0, sn = grid.sub_slab(rank)
     if grid.C > 1:
         out = raw_local.new_empty((q, g.Ny, g.Nx))

@@ -34,6 +34,7 @@ EXPORTS = (
     "ifdk_projection_matrix",
     "ifdk_band_rows",
     "ifdk_filter",
+    "ifdk_filter_scatter",
     "ifdk_backproject",
     "ifdk_backproject_alg2",
     "ifdk_reconstruct",
@@ -66,6 +67,12 @@ _lib.ifdk_band_rows.argtypes = [_vp, _i, _i, _l, ctypes.POINTER(_i), ctypes.POIN
 _lib.ifdk_band_rows.restype = _i
 _lib.ifdk_filter.argtypes = [_vp, _vp, _vp, _l, _i, _i, _vp]
 _lib.ifdk_filter.restype = _i
+class _BandDest(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_void_p), ("v_lo", ctypes.c_int), ("v_hi", ctypes.c_int)]
+
+
+_lib.ifdk_filter_scatter.argtypes = [_vp, _vp, _l, _i, _i, _i, ctypes.POINTER(_BandDest), _vp]
+_lib.ifdk_filter_scatter.restype = _i
 _lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp]
 _lib.ifdk_backproject.restype = _i
 _lib.ifdk_backproject_alg2.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _i, _i, _vp]
@@ -158,6 +165,18 @@ def ifdk_filter(g: Geometry, raw, filtered, v0: int = 0, stream=None) -> None:
         raise ValueError("raw and filtered must both be [n_views][n_rows][Nu]")
     _check(_lib.ifdk_filter(g.handle, _dev_f32(raw, "raw"), _dev_f32(filtered, "filtered"),
                             raw.shape[0], int(v0), raw.shape[1], _stream_ptr(stream)))
+
+
+def ifdk_filter_scatter(g: Geometry, raw, dests, v0: int = 0, stream=None) -> None:
+    """Alg. alg:filter of raw [n_views][n_rows][Nu] (rows v0..), each filtered row stored into
+    every destination band that holds it.  dests: list of (ptr, v_lo, v_hi) where ptr is a
+    device pointer (int, e.g. tensor.data_ptr() or a peer-mapped symmetric-memory address) to
+    an [n_views][v_hi - v_lo + 1][Nu] fp32 buffer."""
+    if raw.dim() != 3 or raw.shape[2] != g.Nu:
+        raise ValueError("raw must be [n_views][n_rows][Nu]")
+    arr = (_BandDest * len(dests))(*[_BandDest(int(b), int(lo), int(hi)) for b, lo, hi in dests])
+    _check(_lib.ifdk_filter_scatter(g.handle, _dev_f32(raw, "raw"), raw.shape[0], int(v0),
+                                    raw.shape[1], len(dests), arr, _stream_ptr(stream)))
 
 
 def ifdk_backproject(g: Geometry, filtered, s0: int, vol, k0: int = 0, v0: int = 0,

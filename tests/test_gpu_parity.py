@@ -68,6 +68,30 @@ def test_filter_matches_oracle(torch_cuda, Nu, n_rows, n_views, v0):
     assert torch.equal(raw, out)
 
 
+@pytest.mark.parametrize("Nu,Nv,n_views,bands", [
+    (2048, 40, 3, [(0, 39), (5, 17), (17, 30), (39, 39)]),  # f4k kernel; overlapping bands
+    (100, 24, 5, [(3, 9), (0, 23)]),                          # generic kernel, odd row total
+])
+def test_filter_scatter_equals_filter_then_slice(torch_cuda, Nu, Nv, n_views, bands):
+    """The fused filter + band scatter (the k-slab exchange riding the filter) stores exactly
+    ifdk_filter's values, row band by row band, and nothing else."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_filter, ifdk_filter_scatter
+
+    spec = _spec(64, Nu, Nv, 32, 32, 32)
+    g = Geometry.from_spec(spec)
+    rng = np.random.default_rng(Nu)
+    raw = torch.from_numpy((np.abs(rng.standard_normal((n_views, Nv, Nu))) * 20)
+                           .astype(np.float32)).cuda()
+    Q = torch.empty_like(raw)
+    ifdk_filter(g, raw, Q)
+    outs = [torch.full((n_views, hi - lo + 1, Nu), float("nan"), device="cuda")
+            for lo, hi in bands]
+    ifdk_filter_scatter(g, raw, [(o.data_ptr(), lo, hi) for o, (lo, hi) in zip(outs, bands)])
+    for o, (lo, hi) in zip(outs, bands):
+        assert torch.equal(o, Q[:, lo:hi + 1]), (lo, hi)
+
+
 def test_filter_phantom_config1(torch_cuda):
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_filter
