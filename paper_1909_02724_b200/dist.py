@@ -217,16 +217,16 @@ def _p2p_buffers(group, numel, dev):
     key = (id(pg), numel, str(dev))
     if key in _P2P_CACHE:
         return _P2P_CACHE[key]
-    hdl = None
+    hdl, buf = None, None
     try:
         import torch.distributed._symmetric_memory as symm_mem
 
-        if hasattr(symm_mem, "enable_symm_mem_for_group"):
-            symm_mem.enable_symm_mem_for_group(pg.group_name)
         buf = symm_mem.empty(numel, dtype=torch.float32, device=dev)
         hdl = symm_mem.rendezvous(buf, pg)
-        hdl._ifdk_keepalive = buf
-    except Exception:  # noqa: BLE001 -- no P2P/symmetric memory: the NCCL exchange is used
+    except Exception as exc:  # noqa: BLE001 -- no P2P/symmetric memory: the NCCL exchange
+        import warnings
+
+        warnings.warn(f"symmetric memory unavailable, NCCL band exchange: {exc!r}")
         hdl = None
     # every rank must take the same path
     ok = torch.tensor([1 if hdl is not None else 0], device=dev)
@@ -234,6 +234,7 @@ def _p2p_buffers(group, numel, dev):
     if int(ok.item()) == 0:
         hdl = None
     _P2P_CACHE[key] = hdl
+    _P2P_CACHE[key + ("buffer",)] = buf  # the handle does not own the allocation
     return hdl
 
 

@@ -24,3 +24,5 @@ def test_kslab_under_torchrun_both_exchanges():
     print(out[-3000:])
     assert r.returncode == 0, out[-3000:]
     assert out.count("bitwise=OK") == 2 * n, out[-3000:]
+    # on B200 the default exchange is the fused filter + symmetric-memory scatter
+    assert out.count("exchange=auto used=p2p-fused") == n, out[-3000:]
