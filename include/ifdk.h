@@ -155,6 +155,42 @@ ifdk_status ifdk_backproject_alg2(const ifdk_geometry* g, const float* filtered_
                                   long n_views, float* vol_dev, int k0, int nk, int accumulate,
                                   int texture, void* stream);
 
+/* ---- iterative reconstruction (SART / SIRT) ---- */
+
+/* The matched forward projector: the exact transpose of ifdk_backproject
+ * (Alg. alg:bp + alg:subpixel; reading c-I1).  For views s0..s0+n_views-1,
+ *   proj_dev[t][v-v0][u] (=|+=) sum over the slab k0..k0+nk-1 of
+ *                               f^2 . w_(u,v)(x f, y f) . vol_dev[k-k0][j][i],
+ * [x,y,z] = P_s.[i,j,k,1], f = 1/z, w the bilinear weight of detector tap (u,v) in
+ * Alg. alg:subpixel (0 unless (u,v) is one of the four taps).  Taps off the
+ * detector are dropped (reading c-A9).  vol_dev: [nk][Ny][Nx] fp32 device;
+ * proj_dev: [n_views][n_rows][Nu] fp32 device holding rows v0..v0+n_rows-1, which
+ * must cover ifdk_band_rows(k0,nk,s) for every view, else SHAPE (a dropped tap
+ * would break the adjoint).  accumulate = 0 overwrites the band, 1 adds to it.
+ * The sums are order-dependent fp32 atomics: not bitwise reproducible.
+ * Errors: INVALID_ARGUMENT (NULL, accumulate not 0/1), SHAPE (as ifdk_backproject). */
+ifdk_status ifdk_forward_project(const ifdk_geometry* g, const float* vol_dev, int k0, int nk,
+                                 long s0, long n_views, float* proj_dev, int v0, int n_rows,
+                                 int accumulate, void* stream);
+
+/* SART residual step (reading c-I2): out[e] = (b[e] - ax[e]) / R[e], 0 where
+ * R[e] <= 0 (rays no voxel reaches, reading c-I3).  R = forward projection of a
+ * volume of ones.  n elements, fp32 device; out may alias ax.
+ * Errors: INVALID_ARGUMENT (NULL), SHAPE (n < 0). */
+ifdk_status ifdk_sart_ratio(const float* b_dev, const float* ax_dev, const float* R_dev,
+                            float* out_dev, long n, void* stream);
+
+/* SART update step (reading c-I2): x[e] += lambda c[e] / C[e], unchanged where
+ * C[e] <= 0 (voxels no ray sees, reading c-I3); nonneg = 1 then clamps x at 0.
+ * c = back-projection of the residual ratio, C = back-projection of ones.
+ * Errors: INVALID_ARGUMENT (NULL, lambda outside (0, 2), nonneg not 0/1), SHAPE. */
+ifdk_status ifdk_sart_update(float* x_dev, const float* c_dev, const float* C_dev, float lambda,
+                             long n, int nonneg, void* stream);
+
+/* x[e] = value for n fp32 device elements (normaliser inputs of SART).
+ * Errors: INVALID_ARGUMENT (NULL), SHAPE (n < 0). */
+ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream);
+
 /* Number of device kernels the last successful call on this thread launched. */
 int ifdk_last_launch_count(void);
 

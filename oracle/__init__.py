@@ -19,6 +19,11 @@ What it computes (all fp64; the only fp32 quantity is the raw input E):
 * ``backproject``        -- Alg. alg:bp on a voxel list or a
   k-slab of the volume.
 * ``reconstruct``        -- filter then back-project (the FDK of P:366-454).
+* ``forward_project``    -- the matched forward projector, the transpose of
+  Alg. alg:bp + alg:subpixel (reading c-I1); pinned by the adjoint identity
+  against ``backproject_volume`` and by closed forms.
+* ``sart``               -- SART / SIRT (Andersen & Kak, cited at P:266;
+  readings c-I2, c-I3) built from the two operators.
 
 Parity pins live in ``tests/test_oracle_pins.py``.  Functions whose result
 the paper does not fix (the F_cos formula, the ramp shape, the constant C,
@@ -34,9 +39,11 @@ from .oracle import (  # noqa: F401
     fdk_scale,
     filter_direct,
     filter_fft,
+    forward_project,
     interp2,
     num_threads,
     projection_matrix,
     ramp_h1,
     reconstruct,
+    sart,
 )

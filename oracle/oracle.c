@@ -208,6 +208,59 @@ int oracle_backproject_volume(const oracle_geom *g, const double *Q, long s0, lo
     return st;
 }
 
+/* The matched forward projector (reading c-I1): the transpose of Alg. alg:bp +
+ * alg:subpixel.  Back-projection is V = sum_s sum_taps W w_tap Q_s[tap] (lines
+ * 6-10 with interp2 written as its four weighted taps), so its transpose adds
+ * W * w_tap * vol(i,j,k) into every tap of every voxel's projection:
+ *   out[t][b - v0][a] = sum_{i,j,k} f^2 w_(a,b)(x f, y f) vol[k - k0][j][i],
+ * with w_(a,b) the bilinear weight of tap (a, b) in Alg. alg:subpixel (t1, t2
+ * and the final lerp multiplied out), taps off the detector dropped (c-A9).
+ * vol: [nk][Ny][Nx] slab k0..k0+nk-1 (fp64); out: [n_views][n_rows][Nu] fp64,
+ * rows v0 .. v0+n_rows-1, overwritten.  Views in parallel, voxels in order.
+ * Returns ORACLE_ERR_BAND if a tap on the detector falls outside the band. */
+int oracle_forward_project(const oracle_geom *g, const double *vol, int k0, int nk, long s0,
+                           long n_views, int v0, int n_rows, double *out)
+{
+    int missing_any = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : missing_any)
+    for (long t = 0; t < n_views; ++t) {
+        double P[12];
+        oracle_projection_matrix(g, s0 + t, P);
+        double *o = out + t * (long)n_rows * g->Nu;
+        for (long e = 0; e < (long)n_rows * g->Nu; ++e) o[e] = 0.0;
+        for (int k = k0; k < k0 + nk; ++k)
+            for (int j = 0; j < g->Ny; ++j)
+                for (int i = 0; i < g->Nx; ++i) {
+                    const double val = vol[((long)(k - k0) * g->Ny + j) * g->Nx + i];
+                    const double x = P[0] * i + P[1] * j + P[2] * k + P[3];
+                    const double y = P[4] * i + P[5] * j + P[6] * k + P[7];
+                    const double z = P[8] * i + P[9] * j + P[10] * k + P[11];
+                    const double f = 1.0 / z;
+                    const double W = f * f; /* line 8 */
+                    const double u = x * f, v = y * f;
+                    const double fu = floor(u), fv = floor(v); /* c-A8 */
+                    const long nu = (long)fu, nv = (long)fv;
+                    const double du = u - fu, dv = v - fv;
+                    /* interp2 = T(nu,nv)(1-du)(1-dv) + T(nu+1,nv) du(1-dv)
+                     *         + T(nu,nv+1)(1-du) dv + T(nu+1,nv+1) du dv */
+                    const long ta[4] = {nu, nu + 1, nu, nu + 1};
+                    const long tb[4] = {nv, nv, nv + 1, nv + 1};
+                    const double w[4] = {(1.0 - du) * (1.0 - dv), du * (1.0 - dv),
+                                         (1.0 - du) * dv, du * dv};
+                    for (int q = 0; q < 4; ++q) {
+                        const long a = ta[q], b = tb[q];
+                        if (a < 0 || a >= g->Nu || b < 0 || b >= g->Nv) continue; /* c-A9 */
+                        if (b < v0 || b >= (long)v0 + n_rows) {
+                            if (w[q] * val != 0.0) missing_any = 1;
+                            continue;
+                        }
+                        o[(b - v0) * (long)g->Nu + a] += W * w[q] * val;
+                    }
+                }
+    }
+    return missing_any ? ORACLE_ERR_BAND : ORACLE_OK;
+}
+
 int oracle_num_threads(void)
 {
 #ifdef _OPENMP

@@ -87,6 +87,9 @@ def _L():
                                                    ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                    ctypes.c_int, dp]
         _lib.oracle_backproject_volume.restype = ctypes.c_int
+        _lib.oracle_forward_project.argtypes = [g, dp, ctypes.c_int, ctypes.c_int, ctypes.c_long,
+                                                ctypes.c_long, ctypes.c_int, ctypes.c_int, dp]
+        _lib.oracle_forward_project.restype = ctypes.c_int
         _lib.oracle_num_threads.restype = ctypes.c_int
     return _lib
 
@@ -212,3 +215,47 @@ def reconstruct(g: OracleGeometry, E: np.ndarray, s0: int = 0, fft: bool = False
     """FDK = Alg. alg:filter then Alg. alg:bp over the whole volume ([Nz][Ny][Nx] fp64)."""
     Q = filter_fft(g, E) if fft else filter_direct(g, E)
     return backproject_volume(g, Q, s0=s0)
+
+
+def forward_project(g: OracleGeometry, vol: np.ndarray, s0: int = 0, n_views: int = 1,
+                    v0: int = 0, n_rows: int | None = None, k0: int = 0) -> np.ndarray:
+    """The matched forward projector (reading c-I1, the transpose of Alg. alg:bp +
+    alg:subpixel) of the slab vol [nk][Ny][Nx] (k0..): returns [n_views][n_rows][Nu] fp64."""
+    if n_rows is None:
+        n_rows = g.Nv - v0
+    vol = np.ascontiguousarray(vol, dtype=np.float64)
+    out = np.empty((n_views, n_rows, g.Nu), np.float64)
+    cg = g.c()
+    st = _L().oracle_forward_project(ctypes.byref(cg), _ptr(vol, ctypes.c_double), int(k0),
+                                     vol.shape[0], int(s0), int(n_views), int(v0), int(n_rows),
+                                     _ptr(out, ctypes.c_double))
+    if st != 0:
+        raise BandError("a tap on the detector is outside the supplied row band")
+    return out
+
+
+def sart(g: OracleGeometry, b: np.ndarray, n_iter: int, lam: float = 1.0,
+         block: int | None = None, x0: np.ndarray | None = None,
+         nonneg: bool = False) -> np.ndarray:
+    """SART / SIRT (Andersen & Kak, cited at P:266; reading c-I2), written out step by step:
+    for each iteration and each subset S of `block` consecutive views (block = all views:
+    SIRT),  x <- x + lam * M_S^T((b_S - M_S x) / R_S) / C_S  with R_S = M_S 1 (row sums),
+    C_S = M_S^T 1 (column sums), M_S the forward projector of the views of S and M_S^T the
+    back-projector (Alg. alg:bp).  Zero normalisers leave the term out (reading c-I3).
+    b: [Np][Nv][Nu] for views 0..Np-1.  Returns x [Nz][Ny][Nx] fp64."""
+    Np = b.shape[0]
+    block = block or Np
+    x = np.zeros((g.Nz, g.Ny, g.Nx)) if x0 is None else np.array(x0, dtype=np.float64)
+    ones_vol = np.ones((g.Nz, g.Ny, g.Nx))
+    for _ in range(n_iter):
+        for s0 in range(0, Np, block):
+            n = min(block, Np - s0)
+            R = forward_project(g, ones_vol, s0, n)
+            C = backproject_volume(g, np.ones((n, g.Nv, g.Nu)), s0=s0)
+            resid = b[s0:s0 + n] - forward_project(g, x, s0, n)
+            ratio = np.where(R > 0, resid / np.where(R > 0, R, 1.0), 0.0)
+            c = backproject_volume(g, ratio, s0=s0)
+            x = x + np.where(C > 0, lam * c / np.where(C > 0, C, 1.0), 0.0)
+            if nonneg:
+                x = np.maximum(x, 0.0)
+    return x

@@ -3,7 +3,8 @@
 The compute lives in ``libifdk.so`` (hand-written sm_100a CUDA behind the C ABI
 of ``include/ifdk.h``); ``ifdk`` is its thin ctypes binding and ``dist`` the
 multi-GPU drivers (k-slab split with row-band exchange, projection split with
-reduce-scatter) over ``torch.distributed``.
+reduce-scatter) over ``torch.distributed``; ``iterative`` runs SART / SIRT from the
+back-projector and its transpose, the matched forward projector.
 """
 from .ifdk import (  # noqa: F401
     Geometry,
@@ -11,8 +12,13 @@ from .ifdk import (  # noqa: F401
     ifdk_backproject,
     ifdk_backproject_alg2,
     ifdk_filter,
+    ifdk_fill,
     ifdk_filter_scatter,
+    ifdk_forward_project,
     ifdk_reconstruct,
     ifdk_reconstruct_host,
+    ifdk_sart_ratio,
+    ifdk_sart_update,
     last_launch_count,
 )
+from .iterative import SART, sart  # noqa: F401

@@ -139,6 +139,72 @@ extern "C" ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* fil
                               accumulate, (cudaStream_t)stream);
 }
 
+extern "C" ifdk_status ifdk_forward_project(const ifdk_geometry* g, const float* vol_dev, int k0,
+                                            int nk, long s0, long n_views, float* proj_dev,
+                                            int v0, int n_rows, int accumulate, void* stream)
+{
+    t_launches = 0;
+    if (!g || !vol_dev || (!proj_dev && n_views > 0))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (accumulate != 0 && accumulate != 1)
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "accumulate must be 0 or 1");
+    ifdk_status s = check_band(g, n_views, v0, n_rows);
+    if (s != IFDK_OK) return s;
+    if (k0 < 0 || nk < 1 || (long)k0 + nk > g->Nz)
+        return fail(IFDK_ERR_SHAPE, "slab k0..k0+nk-1 outside [0, Nz)");
+    for (long t = 0; t < n_views; ++t) {
+        int lo, hi;
+        band_rows(g, k0, nk, s0 + t, &lo, &hi);
+        if (lo <= hi && (lo < v0 || hi > v0 + n_rows - 1)) {
+            char buf[200];
+            snprintf(buf, sizeof buf,
+                     "view %ld reaches detector rows %d..%d but the band holds %d..%d", s0 + t,
+                     lo, hi, v0, v0 + n_rows - 1);
+            return fail(IFDK_ERR_SHAPE, buf);
+        }
+    }
+    if ((s = need_device()) != IFDK_OK) return s;
+    return launch_forward_project(g, vol_dev, k0, nk, s0, n_views, proj_dev, v0, n_rows,
+                                  accumulate, (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_sart_ratio(const float* b_dev, const float* ax_dev, const float* R_dev,
+                                       float* out_dev, long n, void* stream)
+{
+    t_launches = 0;
+    if (n < 0) return fail(IFDK_ERR_SHAPE, "n < 0");
+    if (n > 0 && (!b_dev || !ax_dev || !R_dev || !out_dev))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    return launch_sart_ratio(b_dev, ax_dev, R_dev, out_dev, n, (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_sart_update(float* x_dev, const float* c_dev, const float* C_dev,
+                                        float lambda, long n, int nonneg, void* stream)
+{
+    t_launches = 0;
+    if (n < 0) return fail(IFDK_ERR_SHAPE, "n < 0");
+    if (n > 0 && (!x_dev || !c_dev || !C_dev))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (!(lambda > 0.f && lambda < 2.f))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "relaxation lambda must lie in (0, 2)");
+    if (nonneg != 0 && nonneg != 1) return fail(IFDK_ERR_INVALID_ARGUMENT, "nonneg must be 0 or 1");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    return launch_sart_update(x_dev, c_dev, C_dev, lambda, n, nonneg, (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream)
+{
+    t_launches = 0;
+    if (n < 0) return fail(IFDK_ERR_SHAPE, "n < 0");
+    if (n > 0 && !x_dev) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    return launch_fill(x_dev, value, n, (cudaStream_t)stream);
+}
+
 extern "C" ifdk_status ifdk_backproject_alg2(const ifdk_geometry* g, const float* filtered_dev,
                                              long s0, long n_views, float* vol_dev, int k0, int nk,
                                              int accumulate, int texture, void* stream)

@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -34,21 +35,13 @@
 #include <vector>
 
 #include "ifdk_internal.h"
+#include "kwalk.cuh"
 
 namespace ifdk {
 namespace {
 
 constexpr int kTI = 16, kTJ = 16, kThreads = 256;
-
-// Views per launch: their projection matrices ride in the kernel's parameter space
-// (20 KB of the 32 KB parameter limit).  A multiple of the summation batch vb = 128.
-constexpr int kMaxViewsPerLaunch = 256;
-
-// The used entries of P_s (P[0][2] = P[2][2] = 0, Theorems 2-3):
-// P00 P01 P03 | P10 P11 P12 P13 | P20 P21 P23
-struct PTable {
-    double P[kMaxViewsPerLaunch][10];
-};
+constexpr int kRasterTiles = 16;  // tile columns per raster band (see bp_kernel)
 
 struct BPParams {
     const float* Q;   // band [n_views][n_rows][Nu]
@@ -60,6 +53,7 @@ struct BPParams {
     int k0, nk;       // slab (global k)
     int kb0;          // global k of chunk 0 (multiple of KC)
     int tiles_i;
+    int raster;       // tile columns per raster band (see bp_kernel)
     int box_w, box_h;
     int raw_bytes;    // bytes of one raw box (multiple of 128)
     int vb;           // view batch of the two-level summation
@@ -124,55 +118,6 @@ __device__ __forceinline__ float2 lds64(uint32_t addr)
     float2 v;
     asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
     return v;
-}
-
-// Per-(column, view) invariants in fp64 (Theorems 2-3): u and 1/z are k-invariant; v at the
-// chunk base kb; dv = dv/dk.  Shared by the threads and by the patch-bound computation so
-// that corner columns reproduce the threads' values bit for bit.
-struct ColInv {
-    double u, v, f, dv;
-};
-
-__device__ __forceinline__ ColInv column_invariants(const double* P, double i, double j, double kb)
-{
-    ColInv c;
-    const double x = fma(P[0], i, fma(P[1], j, P[2]));
-    const double y = fma(P[3], i, fma(P[4], j, fma(P[5], kb, P[6])));
-    const double z = fma(P[7], i, fma(P[8], j, P[9]));
-    c.f = __drcp_rn(z);
-    c.u = x * c.f;
-    c.v = y * c.f;
-    c.dv = P[5] * c.f;
-    return c;
-}
-
-// Thread-side split of the invariants: integer detector column/row + fp32 fractions.
-struct ThreadInv {
-    int nu, nv;
-    float du, fv0, dv, dvm1, W;
-};
-
-__device__ __forceinline__ ThreadInv split(const ColInv& c)
-{
-    ThreadInv t;
-    const double fu = floor(c.u), fv = floor(c.v);
-    t.nu = (int)fu;
-    t.nv = (int)fv;
-    t.du = (float)(c.u - fu);
-    t.fv0 = (float)(c.v - fv);
-    t.dv = (float)c.dv;
-    t.dvm1 = t.dv - 1.f;
-    t.W = (float)(c.f * c.f);  // W_dis = f^2, Alg. alg:bp line 8
-    return t;
-}
-
-// floor() of a non-negative fp32 v < 2^23 through the round-down magic add: the returned
-// bits are 0x4B000000 + floor(v); *fr = v - floor(v) exactly.
-__device__ __forceinline__ uint32_t floor_bits(float v, float* fr)
-{
-    const float t = __fadd_rd(v, 8388608.0f);
-    *fr = v - (t - 8388608.0f);
-    return __float_as_uint(t);
 }
 
 // One view from the (a, delta) pair patch in shared memory.
@@ -293,6 +238,135 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
     }
 }
 
+// ---- PAIR walk on packed fp32x2 (Blackwell FFMA2 / FADD2): WALK == 4 ------------------
+// The arithmetic of the WALK == 2 PAIR walk, element for element (same operations, same
+// rounding), issued two slice pairs at a time: slice pair A = (kk, kk+1) in the low halves,
+// B = (kk+2, kk+3) in the high halves.  v, the floor, the fractions, the row differences,
+// the vertical lerps and the accumulation run as f32x2 instructions; only the address IMAD,
+// the shared loads, the horizontal lerps (operands arrive as (a, delta) pairs of one row) and
+// the row select stay scalar: 29 instructions per 4 updates instead of 38.  The accumulators
+// are register pairs: acc2[kk/2] = (slice kk, slice kk+2), acc2[kk/2+1] = (kk+1, kk+3).
+using f2x = unsigned long long;
+
+__device__ __forceinline__ f2x pk2(float lo, float hi)
+{
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float lo2(f2x r)
+{
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float hi2(f2x r)
+{
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return b;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c)
+{
+    f2x r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b)
+{
+    f2x r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2x add2_rd(f2x a, f2x b)
+{
+    f2x r;
+    asm("add.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2x sub2(f2x a, f2x b)
+{
+    f2x r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+
+template <int KC, int P2, bool FULL, typename Hook>
+__device__ __forceinline__ void accumulate_view_smem_x2(f2x (&acc)[KC / 2], uint32_t pair_base,
+                                                        uint32_t neg_magic, const ThreadInv& t,
+                                                        int u_org, int v_org, int kv0, int kv1,
+                                                        Hook&& hook)
+{
+    static_assert(KC % 4 == 0, "x2 walk: whole slice quads");
+    const uint32_t a0 =
+        pair_base + (uint32_t)(((t.nv - v_org) * P2 + (t.nu - u_org)) * 8) + neg_magic;
+    constexpr uint32_t S = P2 * 8;
+    const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
+    const f2x magic2 = pk2(8388608.0f, 8388608.0f), nmagic2 = pk2(-8388608.0f, -8388608.0f);
+    f2x fv02 = pk2(t.fv0, t.fv0);
+    // (kk, kk+2) as floats, stepped by an exact FADD2 (kept opaque so that it is not
+    // folded into two uniform-register moves per quad)
+    f2x kpair = pk2(0.f, 2.f);
+    const f2x four2 = pk2(4.f, 4.f);
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+        if ((kk & 7) == 0) {
+            hook(kk >> 3);
+            asm volatile("mov.b64 %0, %0;" : "+l"(fv02));
+        }
+        // v of slices kk (A) and kk+2 (B); floor by the round-down magic add (floor_bits)
+        const f2x v = fma2(kpair, dv2, fv02);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(kpair) : "l"(four2));
+        const f2x tb = add2_rd(v, magic2);
+        const f2x fr = sub2(v, add2(tb, nmagic2));
+        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        const float2 pA0 = lds64(adA), pA1 = lds64(adA + S), pA2 = lds64(adA + 2 * S);
+        const float2 pB0 = lds64(adB), pB1 = lds64(adB + S), pB2 = lds64(adB + 2 * S);
+        // Alg. alg:subpixel lines 4-5 (horizontal), rows n, n+1, n+2 of A and B
+        const f2x h0 = pk2(fmaf(t.du, pA0.y, pA0.x), fmaf(t.du, pB0.y, pB0.x));
+        const f2x h1 = pk2(fmaf(t.du, pA1.y, pA1.x), fmaf(t.du, pB1.y, pB1.x));
+        const f2x h2 = pk2(fmaf(t.du, pA2.y, pA2.x), fmaf(t.du, pB2.y, pB2.x));
+        const f2x d01 = sub2(h1, h0), d12 = sub2(h2, h1);
+        const f2x g = add2(fr, dvm12);  // second slice of each pair: g rows past row n+1
+        const float eA = lo2(g) >= 0.f ? lo2(d12) : lo2(d01);
+        const float eB = hi2(g) >= 0.f ? hi2(d12) : hi2(d01);
+        const f2x val0 = fma2(fr, d01, h0);           // slices kk, kk+2 (line 6)
+        const f2x val1 = fma2(g, pk2(eA, eB), h1);    // slices kk+1, kk+3
+        f2x& a0p = acc[kk / 2];
+        f2x& a1p = acc[kk / 2 + 1];
+        if (FULL) {
+            a0p = fma2(W2, val0, a0p);  // Alg. alg:bp line 10
+            a1p = fma2(W2, val1, a1p);
+        } else {
+            const f2x n0 = fma2(W2, val0, a0p), n1 = fma2(W2, val1, a1p);
+            a0p = pk2((kk >= kv0 && kk < kv1) ? lo2(n0) : lo2(a0p),
+                      (kk + 2 >= kv0 && kk + 2 < kv1) ? hi2(n0) : hi2(a0p));
+            a1p = pk2((kk + 1 >= kv0 && kk + 1 < kv1) ? lo2(n1) : lo2(a1p),
+                      (kk + 3 >= kv0 && kk + 3 < kv1) ? hi2(n1) : hi2(a1p));
+        }
+    }
+}
+
+// Slice kk of the packed accumulators (see accumulate_view_smem_x2).
+template <int KC>
+__device__ __forceinline__ void flush_x2(f2x (&acc)[KC / 2], const BPParams& p, int i, int j,
+                                         int kb, int kv0, int kv1, bool overwrite)
+{
+    float* q = p.vol + ((long)(kb - p.k0) * p.Ny + j) * p.Nx + i;
+    long plane = (long)p.Ny * p.Nx;
+    asm volatile("mov.b64 %0, %0;" : "+l"(plane));
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+        const f2x a = acc[(kk & ~3) / 2 + (kk & 1)];
+        const float v = (kk & 2) ? hi2(a) : lo2(a);
+        if (kk >= kv0 && kk < kv1) *q = overwrite ? v : *q + v;
+        q += plane;
+    }
+#pragma unroll
+    for (int q2 = 0; q2 < KC / 2; ++q2) acc[q2] = 0ull;
+}
+
 __device__ __forceinline__ float tapg(const float* __restrict__ Qv, int Nu, int Nv, int v0,
                                       int n_rows, int row, int col)
 {
@@ -347,6 +421,16 @@ __device__ __forceinline__ void accumulate_view_global(float (&acc)[KC], const f
     }
 }
 
+// Register accumulators of a thread's KC slices: scalar, or fp32x2 pairs for WALK == 4.
+template <int KC, bool X2>
+struct AccRegs {
+    float a[KC];
+};
+template <int KC>
+struct AccRegs<KC, true> {
+    f2x a[KC / 2];
+};
+
 template <int KC>
 __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i, int j, int kb,
                                       int kv0, int kv1, bool overwrite)
@@ -370,24 +454,22 @@ __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i
 constexpr int kMetaRing = 16;
 
 template <int KC, int WALK>
-__device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, int t, int i_lo,
-                              int i_hi, int j_lo, int j_hi, int kb, int kv0, int kv1)
+__device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, int t, int i_corner,
+                              int j_corner, int kb, int kv0, int kv1)
 {
     const int lane = threadIdx.x & 31;
-    const int corner = lane & 3;
     double P[10];
 #pragma unroll
     for (int q = 0; q < 10; ++q) P[q] = Pc[q];  // constant bank, warp-uniform address
     Meta* m = &ring[t & (kMetaRing - 1)];
     if (lane < 10) m->P[lane] = Pc[lane];
-    const double ci = (corner & 1) ? i_hi : i_lo;
-    const double cj = (corner & 2) ? j_hi : j_lo;
+    const double ci = i_corner, cj = j_corner;
     const ColInv c = column_invariants(P, ci, cj, (double)kb);
     double umin = c.u, umax = c.u;
     // slices whose rows are read: the PAIR walk reads from the even slice below kv0 to the odd
     // slice at or above kv1 - 1, and one row more (h_need below)
     int ka = kv0, kz = kv1 - 1;
-    if constexpr (WALK == 2) {
+    if constexpr (WALK == 2 || WALK == 4) {
         ka = kv0 & ~1;
         kz = (kv1 - 1) | 1;
     } else if constexpr (WALK == 3) {  // triples start on multiples of 3; the tail is single
@@ -427,23 +509,38 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int tile_i = blockIdx.x % p.tiles_i, tile_j = blockIdx.x / p.tiles_i;
+    // L2-friendly raster: the grid is (raster x tiles_j, chunks, bands of `raster` tile
+    // columns), so consecutive CTAs walk down one band and the ~300 resident CTAs cover a
+    // block of raster x ~300/raster tiles whose detector patches (all views of the launch)
+    // stay in L2; a row-major raster (raster = tiles_i) spans the whole i extent and
+    // re-reads every view's rows from HBM once per wave.  CTAs past the volume edge of the
+    // last band exit.
+    const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
+    const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
+    if (tile_i >= p.tiles_i) return;
     const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
     const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
     const bool active = i < p.Nx && j < p.Ny;
     // Columns past the volume edge shadow the last valid column (branch-free update loop);
     // they never write.
     const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
-    const int i_lo = tile_i * kTI, i_hi = min(i_lo + kTI, p.Nx) - 1;
-    const int j_lo = tile_j * kTJ, j_hi = min(j_lo + kTJ, p.Ny) - 1;
+    // this lane's tile corner for the patch boxes: lane % 4 = corner (i_lo|i_hi, j_lo|j_hi)
+    const int i_corner = (lane & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
+    const int j_corner = (lane & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
     const int kb = p.kb0 + (int)blockIdx.y * KC;
     const double dkb = (double)kb;
     const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, KC);
     const bool full = kv0 == 0 && kv1 == KC;
 
-    float acc[KC];
+    constexpr bool X2 = WALK == 4;
+    AccRegs<KC, X2> acc;
+    if constexpr (X2) {
 #pragma unroll
-    for (int kk = 0; kk < KC; ++kk) acc[kk] = 0.f;
+        for (int q = 0; q < KC / 2; ++q) acc.a[q] = 0ull;
+    } else {
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) acc.a[kk] = 0.f;
+    }
     bool overwrite = !p.accumulate;
     const int n = (int)p.n_views;
 
@@ -498,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     };
     auto metas = [=](int t0) {  // all warps: boxes of views t0 .. t0+7
         if (t0 + warp < n)
-            compute_meta1<KC, WALK>(meta, p, ptab->P[t0 + warp], t0 + warp, i_lo, i_hi, j_lo, j_hi, kb, kv0,
+            compute_meta1<KC, WALK>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner, kb, kv0,
                           kv1);
     };
 
@@ -572,12 +669,21 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
                 }
             };
             const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
-            if (full)
-                accumulate_view_smem<KC, P2, true, WALK>(acc, pb, p.neg_magic, ti, u_org, v_org,
-                                                         kv0, kv1, row);
-            else
-                accumulate_view_smem<KC, P2, false, WALK>(acc, pb, p.neg_magic, ti, u_org, v_org,
-                                                          kv0, kv1, row);
+            if constexpr (X2) {
+                if (full)
+                    accumulate_view_smem_x2<KC, P2, true>(acc.a, pb, p.neg_magic, ti, u_org,
+                                                          v_org, kv0, kv1, row);
+                else
+                    accumulate_view_smem_x2<KC, P2, false>(acc.a, pb, p.neg_magic, ti, u_org,
+                                                           v_org, kv0, kv1, row);
+            } else {
+                if (full)
+                    accumulate_view_smem<KC, P2, true, WALK>(acc.a, pb, p.neg_magic, ti, u_org,
+                                                             v_org, kv0, kv1, row);
+                else
+                    accumulate_view_smem<KC, P2, false, WALK>(acc.a, pb, p.neg_magic, ti, u_org,
+                                                              v_org, kv0, kv1, row);
+            }
             if (nxt) {
                 if (narrow) {
                     for (int q = KC / 8; warp + (kThreads / 32) * q < hn; ++q) row(q);
@@ -586,11 +692,16 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
                 }
             }
         } else {
-            accumulate_view_global<KC, (WALK >= 2)>(acc, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0,
+            if constexpr (!X2)
+                accumulate_view_global<KC, (WALK >= 2)>(acc.a, p.Q + (long)t * p.n_rows * p.Nu, p, ti, kv0,
                                              kv1);
         }
         if (t == next_flush || t == n - 1) {
-            if (active) flush<KC>(acc, p, i, j, kb, kv0, kv1, overwrite);
+            if constexpr (X2) {
+                if (active) flush_x2<KC>(acc.a, p, i, j, kb, kv0, kv1, overwrite);
+            } else {
+                if (active) flush<KC>(acc.a, p, i, j, kb, kv0, kv1, overwrite);
+            }
             overwrite = false;
             next_flush += p.vb;
         }
@@ -644,18 +755,22 @@ bool use_pair(const ifdk_geometry* g)
     return dv_max < 0.999 && !(pe && pe[0] == '0');
 }
 
-// Slices per floor of the k-walk: 2 (PAIR) when dv/dk < 1 for every z (all five configs),
-// else 1.  IFDK_BP_WALK=3 selects the TRIPLE walk where 0.5 <= dv/dk < 1 (configs 1-4): it
-// needs 11 % less shared-memory traffic per update but measured slower on B200 (config 4,
-// 256 views: 1672 GUPS vs 1800 for PAIR), so it is an opt-in variant.  (IFDK_BP_PAIR=0 forces
-// one floor per slice, with 32-slice chunks.)
+// Slices per floor of the k-walk when dv/dk < 1 for every z (all five configs): the PAIR
+// walk, issued on packed fp32x2 instructions (WALK 4, the default) or scalar (WALK 2; bitwise
+// the same values).  IFDK_BP_WALK=2|3|4 overrides: 3 selects the TRIPLE walk where
+// 0.5 <= dv/dk < 1 (configs 1-4), which needs 11 % less shared-memory traffic per update but
+// measured slower on B200 (config 4, 256 views: 1672 GUPS vs 1800 for scalar PAIR).
+// Otherwise 1 (IFDK_BP_PAIR=0 forces one floor per slice, with 32-slice chunks).
+constexpr int kDefaultPairWalk = 4;
+
 int choose_walk(const ifdk_geometry* g)
 {
     if (!use_pair(g)) return 1;
-    int w = 2;
+    int w = kDefaultPairWalk;
     if (const char* e = std::getenv("IFDK_BP_WALK")) {
         const int v = std::atoi(e);
         const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
+        if (v == 2 || v == 4) w = v;
         if (v == 3 && dv_min >= 0.5001) w = 3;
     }
     return w;
@@ -685,16 +800,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
 {
     // Per-view projection matrices (fp64), passed in the kernel's parameter space.
     PTable pt;
-    for (long t = 0; t < n_views; ++t) {
-        double P[12];
-        projection_matrix(g, s0 + t, P);
-        double* o = pt.P[t];
-        o[0] = P[0]; o[1] = P[1]; o[2] = P[3];
-        o[3] = P[4]; o[4] = P[5]; o[5] = P[6]; o[6] = P[7];
-        o[7] = P[8]; o[8] = P[9]; o[9] = P[11];
-    }
-    for (long t = n_views; t < kMaxViewsPerLaunch; ++t)
-        for (int q = 0; q < 10; ++q) pt.P[t][q] = 0.0;
+    fill_ptable(g, s0, n_views, pt);
 
     BPParams p{};
     p.Q = Q;
@@ -749,7 +855,17 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         p.raw_bytes = 0;
     }
     p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
-    dim3 grid((unsigned)(p.tiles_i * tiles_j), (unsigned)n_chunks);
+    // Raster band of 16 tile columns: measured on B200 (config 4, one 256-view launch) DRAM
+    // traffic 49 GB (algorithmic 39 GB) and L2 hit rate 95 %, vs 354 GB and 65 % for the
+    // row-major raster, at the same speed (the kernel is shared-memory bound).
+    // IFDK_BP_RASTER=n overrides (0 = row-major).
+    p.raster = std::min(kRasterTiles, p.tiles_i);
+    if (const char* e = std::getenv("IFDK_BP_RASTER")) {
+        const int r = std::atoi(e);
+        p.raster = (r > 0 && r < p.tiles_i) ? r : p.tiles_i;
+    }
+    dim3 grid((unsigned)(p.raster * tiles_j), (unsigned)n_chunks,
+              (unsigned)((p.tiles_i + p.raster - 1) / p.raster));
     ifdk_status s;
     if (p.walk == 3) {
         switch (P2) {
@@ -757,6 +873,13 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             case 40: s = launch_t<64, 40, 3>(p, map, pt, tma, grid, smem, st); break;
             case 56: s = launch_t<64, 56, 3>(p, map, pt, tma, grid, smem, st); break;
             default: s = launch_t<64, 72, 3>(p, map, pt, tma, grid, smem, st); break;
+        }
+    } else if (p.walk == 4) {
+        switch (P2) {
+            case 24: s = launch_t<64, 24, 4>(p, map, pt, tma, grid, smem, st); break;
+            case 40: s = launch_t<64, 40, 4>(p, map, pt, tma, grid, smem, st); break;
+            case 56: s = launch_t<64, 56, 4>(p, map, pt, tma, grid, smem, st); break;
+            default: s = launch_t<64, 72, 4>(p, map, pt, tma, grid, smem, st); break;
         }
     } else if (p.walk == 2 && KC == 64) {
         switch (P2) {

@@ -1,0 +1,317 @@
+// forward.cu -- the matched forward projector: the exact transpose of BP-sm100 (Alg. alg:bp
+// P:402-430 with Alg. alg:subpixel P:431-447), for iterative reconstruction (SART / SIRT,
+// P:266).
+//
+// Back-projection is V(i,j,k) = sum_s W_s(i,j) sum_taps w_tap(u, v) Q_s[tap], i.e. V = M^T Q
+// with M_s[(v,u),(i,j,k)] = W_s(i,j) w_tap.  Its transpose splats each voxel into the four
+// bilinear taps of its projection:  F_s[tap] = sum_{i,j,k} W_s(i,j) w_tap(u,v) x(i,j,k)
+// (reading c-I1 in DESIGN.md), taps off the detector dropped (the zero border, c-A9).
+//
+// Mapping (the BP kernel's, run backwards): a CTA of 256 threads owns a 16 x 16 column tile
+// and a KC-slice chunk; each thread keeps its column's KC voxel values in registers for the
+// whole launch, computes z, u, W and the base of v in fp64 per view (Theorems 2-3, the same
+// kwalk.cuh code as BP), walks k in fp32 and adds W x w_tap into a shared-memory patch of the
+// detector with shared-memory atomics.  After each view the CTA adds the non-zero part of its
+// patch to the projection in global memory (red.global.add.f32).  The patch is double
+// buffered: the flush of view t and the zeroing for view t+2 overlap the splat of view t+1.
+// Summation order is that of the atomics, so the result is not bitwise reproducible (fp32
+// rounding differences only).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+
+#include "ifdk_internal.h"
+#include "kwalk.cuh"
+
+namespace ifdk {
+namespace {
+
+constexpr int kTI = 16, kTJ = 16, kThreads = 256, kKC = 32;
+
+struct FPParams {
+    const float* vol;  // slab [nk][Ny][Nx]
+    float* proj;       // band [n_views][n_rows][Nu]
+    int n_views;
+    int Nu, Nv, Nx, Ny;
+    int v0, n_rows;
+    int k0, nk;
+    int kb0;           // global k of chunk 0 (multiple of kKC)
+    int tiles_i, raster;
+    int box_w, box_h;  // patch capacity (columns, rows)
+    float qfactor;     // bound on a patch pixel's sum per unit |x|: 256 (1/dv_min + 1) / zmin^2
+};
+
+struct __align__(16) Box {
+    int u_org, v_org, w, h;
+};
+
+__global__ void __launch_bounds__(kThreads, 2)
+    fp_kernel(const __grid_constant__ FPParams p, const __grid_constant__ PTable pt)
+{
+    extern __shared__ __align__(16) float fsm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
+    const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
+    if (tile_i >= p.tiles_i) return;
+    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    const bool active = i < p.Nx && j < p.Ny;
+    const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
+    const int kb = p.kb0 + (int)blockIdx.y * kKC;
+    const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, kKC);
+    const int cap = p.box_w * p.box_h;
+    Box* const box = reinterpret_cast<Box*>(fsm);  // four slots (t & 3)
+    float* const wmax = fsm + 4 * sizeof(Box) / sizeof(float);  // 8 per-warp maxima
+    int* const patch0 = reinterpret_cast<int*>(wmax + 8);       // two buffers of cap ints
+
+    // this column's voxels (0 outside the slab / volume): x(i, j, kb + kk)
+    float x[kKC];
+    float xmax = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < kKC; ++kk) {
+        const bool in = active && kk >= kv0 && kk < kv1;
+        x[kk] = in ? __ldg(p.vol + ((long)(kb + kk - p.k0) * p.Ny + j) * p.Nx + i) : 0.f;
+        xmax = fmaxf(xmax, fabsf(x[kk]));
+    }
+    // Fixed-point scale of the patch (shared-memory atomics are native only for 32-bit
+    // integers; float adds would be CAS loops): 2^e with  max|x| * qfactor * 2^e < 2^30, so no
+    // patch pixel can overflow, and every contribution keeps >= 19 bits below the largest one.
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    if (lane == 0) wmax[warp] = xmax;
+    __syncthreads();
+    xmax = wmax[0];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) xmax = fmaxf(xmax, wmax[w]);
+    if (xmax == 0.f) return;  // an empty block of the volume adds nothing
+    int ex;
+    frexpf(xmax * p.qfactor, &ex);  // xmax qfactor < 2^ex
+    const float scale = ldexpf(1.f, 30 - ex), inv_scale = ldexpf(1.f, ex - 30);
+    // patch box of view t: lanes 0-3 of warp 0 take the tile's corner columns at both chunk
+    // ends (u, v are linear-fractional in the column position: extremes sit at corners)
+    auto make_box = [&](int t) {
+        if (warp != 0 || t >= p.n_views) return;
+        const int c = lane & 3;
+        const double ci = (c & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
+        const double cj = (c & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
+        const ColInv ci0 = column_invariants(pt.P[t], ci, cj, (double)kb);
+        double umin = ci0.u, umax = ci0.u;
+        double vmin = ci0.v + kv0 * ci0.dv, vmax = ci0.v + (kv1 - 1) * ci0.dv;
+        if (vmin > vmax) { const double q = vmin; vmin = vmax; vmax = q; }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            umin = fmin(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+            umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+            vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+            vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        }
+        if (lane == 0) {
+            Box b;
+            b.u_org = (int)floor(umin) - 1;
+            b.v_org = (int)floor(vmin) - 1;
+            b.w = (int)floor(umax) - b.u_org + 3;
+            b.h = (int)floor(vmax) - b.v_org + 3;
+            if (b.w > p.box_w || b.h > p.box_h) __trap();  // the host bound is conservative
+            box[t & 3] = b;
+        }
+    };
+    // add the patch of view t to the projection (non-zero, on-detector, in-band taps) and
+    // zero what was read, so the buffer is clean for view t+2
+    auto flush = [&](int t) {
+        const Box b = box[t & 3];
+        int* const pa = patch0 + (t & 1) * cap;
+        float* const pv = p.proj + (long)t * p.n_rows * p.Nu;
+        for (int e = tid; e < b.h * p.box_w; e += kThreads) {
+            const int r = e / p.box_w, c = e - r * p.box_w;
+            const int q = pa[e];
+            pa[e] = 0;
+            const int col = b.u_org + c, row = b.v_org + r;
+            if (q != 0 && c < b.w && col >= 0 && col < p.Nu && row >= p.v0 &&
+                row < p.v0 + p.n_rows)
+                atomicAdd(pv + (long)(row - p.v0) * p.Nu + col, (float)q * inv_scale);
+        }
+    };
+
+    for (int e = tid; e < 2 * cap; e += kThreads) patch0[e] = 0;
+    make_box(0);
+    __syncthreads();
+    // One barrier per view: splat view t into buffer t & 1 while view t-1's buffer is flushed
+    // and the box of view t+1 is computed.
+    for (int t = 0; t < p.n_views; ++t) {
+        const Box b = box[t & 3];
+        int* const pa = patch0 + (t & 1) * cap;
+        const ThreadInv ti = split(column_invariants(pt.P[t], di, dj, (double)kb));
+        int* const base = pa + (ti.nv - b.v_org) * p.box_w + (ti.nu - b.u_org);
+        const float ws1 = ti.du * scale, ws0 = (1.f - ti.du) * scale;  // columns nu, nu+1
+        // Along k the column's contributions move down the detector rows (v affine in k, dv > 0):
+        // accumulate the (1 - fr) and fr shares of rows cur, cur+1 in registers (A, B) and add
+        // a row to the patch only when the walk leaves it -- two integer atomics per row
+        // instead of four float atomics per slice.
+        if (active) {
+            float fr;
+            int cur = (int)(floor_bits(fmaf((float)kv0, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+            float A = 0.f, B = 0.f;
+            auto add_row = [&](int r, float sv) {  // Alg. alg:subpixel lines 4-5, transposed
+                if (sv != 0.f) {
+                    int* q = base + r * p.box_w;
+                    atomicAdd(q, __float2int_rn(sv * ws0));
+                    atomicAdd(q + 1, __float2int_rn(sv * ws1));
+                }
+            };
+#pragma unroll
+            for (int kk = 0; kk < kKC; ++kk) {
+                if (x[kk] == 0.f) continue;  // outside the slab (and empty voxels)
+                const int n = (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+                if (n != cur) {  // the walk left row cur (n > cur)
+                    add_row(cur, A);
+                    if (n == cur + 1) {
+                        A = B;
+                    } else {
+                        add_row(cur + 1, B);
+                        A = 0.f;
+                    }
+                    B = 0.f;
+                    cur = n;
+                }
+                const float val = ti.W * x[kk];  // W_dis x (Alg. alg:bp line 8, transposed)
+                A = fmaf(val, 1.f - fr, A);      // rows n, n+1 (line 6)
+                B = fmaf(val, fr, B);
+            }
+            add_row(cur, A);
+            add_row(cur + 1, B);
+        }
+        if (t > 0) flush(t - 1);
+        make_box(t + 1);
+        __syncthreads();
+    }
+    if (p.n_views > 0) flush(p.n_views - 1);
+}
+
+}  // namespace
+
+ifdk_status launch_forward_project(const ifdk_geometry* g, const float* vol, int k0, int nk,
+                                   long s0, long n_views, float* proj, int v0, int n_rows,
+                                   int accumulate, cudaStream_t st)
+{
+    cudaError_t e;
+    if (!accumulate && n_views > 0) {
+        e = cudaMemsetAsync(proj, 0, sizeof(float) * (size_t)n_views * n_rows * g->Nu, st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    }
+    if (n_views == 0 || nk == 0) return IFDK_OK;
+    FPParams p{};
+    p.vol = vol;
+    p.Nu = g->Nu; p.Nv = g->Nv; p.Nx = g->Nx; p.Ny = g->Ny;
+    p.v0 = v0; p.n_rows = n_rows;
+    p.k0 = k0; p.nk = nk;
+    p.kb0 = (k0 / kKC) * kKC;
+    p.tiles_i = (g->Nx + kTI - 1) / kTI;
+    const int tiles_j = (g->Ny + kTJ - 1) / kTJ;
+    const int n_chunks = (k0 + nk - p.kb0 + kKC - 1) / kKC;
+    p.raster = std::min(16, p.tiles_i);
+    double wb, hb;
+    patch_bound(g, kTI, kTJ, kKC, &wb, &hb);
+    p.box_w = (int)std::ceil(wb) + 6;
+    p.box_h = (int)std::ceil(hb) + 6;
+    const size_t smem = sizeof(int) * 2 * (size_t)p.box_w * p.box_h + 4 * sizeof(Box) + 8 * sizeof(float);
+    const double dv_min = g->D * g->Dz / (g->Dv * g->zmax);
+    p.qfactor = (float)(256.0 * (1.0 / dv_min + 1.0) / (g->zmin * g->zmin));
+    if (smem > 200 * 1024) return fail(IFDK_ERR_INVALID_ARGUMENT, "forward projector patch too large");
+    e = cudaFuncSetAttribute(fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fp)");
+    dim3 grid((unsigned)(p.raster * tiles_j), (unsigned)n_chunks,
+              (unsigned)((p.tiles_i + p.raster - 1) / p.raster));
+    PTable pt;
+    for (long t = 0; t < n_views; t += kMaxViewsPerLaunch) {
+        const long n = std::min<long>(kMaxViewsPerLaunch, n_views - t);
+        fill_ptable(g, s0 + t, n, pt);
+        p.n_views = (int)n;
+        p.proj = proj + (size_t)t * n_rows * g->Nu;
+        fp_kernel<<<grid, kThreads, smem, st>>>(p, pt);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "fp_kernel launch");
+        count_launch();
+    }
+    return IFDK_OK;
+}
+
+}  // namespace ifdk
+
+// ---- element-wise steps of SART / SIRT (reading c-I2) ---------------------------------------
+namespace ifdk {
+namespace {
+
+__global__ void sart_ratio_kernel(const float* __restrict__ b, const float* ax,
+                                  const float* __restrict__ R, float* out, long n)
+{
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n;
+         e += (long)gridDim.x * blockDim.x) {
+        const float r = R[e];
+        out[e] = r > 0.f ? (b[e] - ax[e]) / r : 0.f;  // rays no voxel reaches: 0 (c-I3)
+    }
+}
+
+__global__ void sart_update_kernel(float* x, const float* __restrict__ c,
+                                   const float* __restrict__ C, float lam, long n, int nonneg)
+{
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n;
+         e += (long)gridDim.x * blockDim.x) {
+        const float w = C[e];
+        float v = x[e] + (w > 0.f ? lam * c[e] / w : 0.f);  // voxels no ray sees: kept (c-I3)
+        if (nonneg) v = fmaxf(v, 0.f);
+        x[e] = v;
+    }
+}
+
+__global__ void fill_kernel(float* x, float value, long n)
+{
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n;
+         e += (long)gridDim.x * blockDim.x)
+        x[e] = value;
+}
+
+unsigned elementwise_grid(long n)
+{
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long blocks = (n + 255) / 256;
+    return (unsigned)std::max(1L, std::min(blocks, (long)sms * 8));
+}
+
+}  // namespace
+
+ifdk_status launch_sart_ratio(const float* b, const float* ax, const float* R, float* out, long n,
+                              cudaStream_t st)
+{
+    if (n == 0) return IFDK_OK;
+    sart_ratio_kernel<<<elementwise_grid(n), 256, 0, st>>>(b, ax, R, out, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "sart_ratio_kernel launch");
+    count_launch();
+    return IFDK_OK;
+}
+
+ifdk_status launch_sart_update(float* x, const float* c, const float* C, float lam, long n,
+                               int nonneg, cudaStream_t st)
+{
+    if (n == 0) return IFDK_OK;
+    sart_update_kernel<<<elementwise_grid(n), 256, 0, st>>>(x, c, C, lam, n, nonneg);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "sart_update_kernel launch");
+    count_launch();
+    return IFDK_OK;
+}
+
+ifdk_status launch_fill(float* x, float value, long n, cudaStream_t st)
+{
+    if (n == 0) return IFDK_OK;
+    fill_kernel<<<elementwise_grid(n), 256, 0, st>>>(x, value, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fill_kernel launch");
+    count_launch();
+    return IFDK_OK;
+}
+
+}  // namespace ifdk

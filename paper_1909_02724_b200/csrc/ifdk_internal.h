@@ -64,6 +64,17 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
                                cudaStream_t st);
 
+// forward.cu: the matched forward projector (transpose of launch_backproject) and the
+// element-wise SART / SIRT steps
+ifdk_status launch_forward_project(const ifdk_geometry* g, const float* vol, int k0, int nk,
+                                   long s0, long n_views, float* proj, int v0, int n_rows,
+                                   int accumulate, cudaStream_t st);
+ifdk_status launch_sart_ratio(const float* b, const float* ax, const float* R, float* out, long n,
+                              cudaStream_t st);
+ifdk_status launch_sart_update(float* x, const float* c, const float* C, float lam, long n,
+                               int nonneg, cudaStream_t st);
+ifdk_status launch_fill(float* x, float value, long n, cudaStream_t st);
+
 // baseline.cu (measured baselines, not the production path)
 ifdk_status launch_backproject_alg2(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                     float* vol, int k0, int nk, int accumulate, int hw,

@@ -39,6 +39,10 @@ EXPORTS = (
     "ifdk_backproject_alg2",
     "ifdk_reconstruct",
     "ifdk_reconstruct_host",
+    "ifdk_forward_project",
+    "ifdk_sart_ratio",
+    "ifdk_sart_update",
+    "ifdk_fill",
     "ifdk_last_launch_count",
     "ifdk_last_error",
 )
@@ -81,6 +85,14 @@ _lib.ifdk_reconstruct.argtypes = [_vp, _vp, _l, _vp, _vp]
 _lib.ifdk_reconstruct.restype = _i
 _lib.ifdk_reconstruct_host.argtypes = [_vp, _vp, _l, _vp, _vp]
 _lib.ifdk_reconstruct_host.restype = _i
+_lib.ifdk_forward_project.argtypes = [_vp, _vp, _i, _i, _l, _l, _vp, _i, _i, _i, _vp]
+_lib.ifdk_forward_project.restype = _i
+_lib.ifdk_sart_ratio.argtypes = [_vp, _vp, _vp, _vp, _l, _vp]
+_lib.ifdk_sart_ratio.restype = _i
+_lib.ifdk_sart_update.argtypes = [_vp, _vp, _vp, ctypes.c_float, _l, _i, _vp]
+_lib.ifdk_sart_update.restype = _i
+_lib.ifdk_fill.argtypes = [_vp, ctypes.c_float, _l, _vp]
+_lib.ifdk_fill.restype = _i
 _lib.ifdk_last_launch_count.argtypes = []
 _lib.ifdk_last_launch_count.restype = _i
 _lib.ifdk_last_error.argtypes = []
@@ -238,3 +250,39 @@ def ifdk_reconstruct_host(g: Geometry, raw_host, vol_host, stream=None) -> None:
     if tuple(vs) != (g.Nz, g.Ny, g.Nx):
         raise ValueError("vol_host must be [Nz][Ny][Nx]")
     _check(_lib.ifdk_reconstruct_host(g.handle, rp, rs[0], vp, _stream_ptr(stream)))
+
+
+def ifdk_forward_project(g: Geometry, vol, s0: int, proj, k0: int = 0, v0: int = 0,
+                         accumulate: bool = False, stream=None) -> None:
+    """proj (=|+=) the matched forward projection (transpose of ifdk_backproject) of the slab
+    vol [nk][Ny][Nx] (k0..) for views s0..s0+n-1; proj [n][n_rows][Nu] holds rows v0.."""
+    if proj.dim() != 3 or proj.shape[2] != g.Nu:
+        raise ValueError("proj must be [n_views][n_rows][Nu]")
+    if vol.dim() != 3 or vol.shape[1] != g.Ny or vol.shape[2] != g.Nx:
+        raise ValueError("vol must be [nk][Ny][Nx]")
+    _check(_lib.ifdk_forward_project(g.handle, _dev_f32(vol, "vol"), int(k0), vol.shape[0],
+                                     int(s0), proj.shape[0], _dev_f32(proj, "proj"), int(v0),
+                                     proj.shape[1], 1 if accumulate else 0, _stream_ptr(stream)))
+
+
+def ifdk_sart_ratio(b, ax, R, out, stream=None) -> None:
+    """out = (b - ax) / R (0 where R <= 0); equal-size float32 CUDA tensors."""
+    n = b.numel()
+    if not (ax.numel() == R.numel() == out.numel() == n):
+        raise ValueError("b, ax, R and out must have the same size")
+    _check(_lib.ifdk_sart_ratio(_dev_f32(b, "b"), _dev_f32(ax, "ax"), _dev_f32(R, "R"),
+                                _dev_f32(out, "out"), n, _stream_ptr(stream)))
+
+
+def ifdk_sart_update(x, c, C, lam: float, nonneg: bool = False, stream=None) -> None:
+    """x += lam c / C (unchanged where C <= 0), optionally clamped at 0."""
+    n = x.numel()
+    if not (c.numel() == C.numel() == n):
+        raise ValueError("x, c and C must have the same size")
+    _check(_lib.ifdk_sart_update(_dev_f32(x, "x"), _dev_f32(c, "c"), _dev_f32(C, "C"),
+                                 float(lam), n, 1 if nonneg else 0, _stream_ptr(stream)))
+
+
+def ifdk_fill(x, value: float, stream=None) -> None:
+    """x[:] = value on the device."""
+    _check(_lib.ifdk_fill(_dev_f32(x, "x"), float(value), x.numel(), _stream_ptr(stream)))

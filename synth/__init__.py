@@ -15,6 +15,7 @@ from .synth import (  # noqa: F401
     default_ellipsoids,
     density,
     ellipsoids,
+    phantom_volume,
     project,
     project_gpu,
     voxel_world,

@@ -207,6 +207,16 @@ def density(ell: np.ndarray, xyz: np.ndarray) -> np.ndarray:
     return out
 
 
+def phantom_volume(spec: ConfigSpec) -> np.ndarray:
+    """The phantom's density sampled at the voxel centres, [Nz][Ny][Nx] fp64: a seeded,
+    structured test volume for the forward projector (no method arithmetic)."""
+    k, j, i = np.meshgrid(np.arange(spec.Nz), np.arange(spec.Ny), np.arange(spec.Nx),
+                          indexing="ij")
+    X, Y, Z = voxel_world(spec, i.ravel(), j.ravel(), k.ravel())
+    rho = density(default_ellipsoids(spec), np.stack([X, Y, Z], axis=1))
+    return rho.reshape(spec.Nz, spec.Ny, spec.Nx)
+
+
 def add_noise(E: np.ndarray, sigma: float, seed: int = 1234, base: int = 0) -> np.ndarray:
     """E + sigma * N(0,1) from a counter-based generator (in place on a copy)."""
     out = np.ascontiguousarray(E, np.float32).copy()

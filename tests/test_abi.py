@@ -114,3 +114,30 @@ def test_compute_entry_points_fail_loudly_without_gpu():
     with pytest.raises(IfdkError) as e:
         ifdk_reconstruct_host(g, raw, vol, stream=0)
     assert e.value.status == 4
+
+
+def test_iterative_entry_points_validate_and_fail_loudly_without_gpu():
+    """ifdk_forward_project / ifdk_sart_* / ifdk_fill: argument errors before any device work,
+    then IFDK_ERR_CUDA without a GPU (no CPU fallback)."""
+    import ctypes
+
+    import torch
+
+    from paper_1909_02724_b200 import Geometry, ifdk
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    lib = ifdk._lib
+    g = Geometry(16, 16, 8, 8, 8, 1.0, 1.0, 1.0, 1.0, 1.0, 40.0, 25.0, 0.1)
+    fake = ctypes.c_void_p(0x1000)
+    # band too small for the slab -> SHAPE; accumulate 2 -> INVALID_ARGUMENT
+    assert lib.ifdk_forward_project(g.handle, fake, 0, 8, 0, 2, fake, 7, 1, 0, None) == 3
+    assert lib.ifdk_forward_project(g.handle, fake, 0, 8, 0, 2, fake, 0, 16, 2, None) == 1
+    assert lib.ifdk_forward_project(g.handle, fake, 0, 9, 0, 2, fake, 0, 16, 0, None) == 3
+    assert lib.ifdk_forward_project(g.handle, fake, 0, 8, 0, 2, fake, 0, 16, 0, None) == 4
+    assert lib.ifdk_sart_update(fake, fake, fake, ctypes.c_float(2.0), 10, 0, None) == 1
+    assert lib.ifdk_sart_update(fake, fake, fake, ctypes.c_float(1.0), -1, 0, None) == 3
+    assert lib.ifdk_sart_update(fake, fake, fake, ctypes.c_float(1.0), 10, 0, None) == 4
+    assert lib.ifdk_sart_ratio(fake, None, fake, fake, 10, None) == 1
+    assert lib.ifdk_sart_ratio(fake, fake, fake, fake, 10, None) == 4
+    assert lib.ifdk_fill(fake, ctypes.c_float(1.0), 10, None) == 4

@@ -183,6 +183,39 @@ def test_bp_slab_split_is_bitwise_and_deterministic(torch_cuda):
             assert torch.equal(slab, full[a:b]), (cuts, a, b)
 
 
+@pytest.mark.parametrize("walk", ["2", "3"])
+def test_bp_walk_variants(torch_cuda, monkeypatch, walk):
+    """The default PAIR walk on packed fp32x2 instructions (WALK 4) gives bitwise the values of
+    the scalar PAIR walk (WALK 2: the same operations and roundings, element by element), on
+    whole chunks and on partial ones (slab cut inside a chunk); the TRIPLE walk (WALK 3)
+    matches the oracle."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    spec = _spec(48, 96, 160, 48, 40, 160)  # dv/dk in [0.60, 0.77]: PAIR and TRIPLE apply
+    g = Geometry.from_spec(spec)
+    Qn = _oracle_Q32(spec, _phantom_E(spec))
+    Q = torch.from_numpy(Qn).cuda()
+
+    def run(w, k0=0, nk=spec.Nz):
+        monkeypatch.setenv("IFDK_BP_WALK", w)
+        vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
+        ifdk_backproject(g, Q, 0, vol, k0=k0)
+        torch.cuda.synchronize()
+        return vol
+
+    x2 = run("4")
+    other = run(walk)
+    if walk == "2":
+        assert torch.equal(x2, other)
+        assert torch.equal(run("4", 77, 54), run("2", 77, 54))
+    else:
+        og = oracle.OracleGeometry(**spec.geometry_args())
+        ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
+        assert_parity(other.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp triple walk")
+        assert_parity(x2.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp x2 walk")
+
+
 def test_bp_view_split_accumulate_matches(torch_cuda):
     """Views in two calls (accumulate) vs one call: equal up to fp32 summation order."""
     torch = torch_cuda
