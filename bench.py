@@ -45,6 +45,8 @@ def parse():
                     help="k-slab band exchange: fused filter + NVLink scatter (auto) or NCCL")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip timing configs 1-3 at N = 1")
+    ap.add_argument("--no-iterative", action="store_true",
+                    help="skip the SIRT iteration timing on config 3")
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the projection-split measurement at N > 1")
     ap.add_argument("--path", default="auto", choices=["auto", "kslab"],
@@ -530,6 +532,45 @@ def run_ours(args, spec, rank, world, local_rank):
             del oraw, ovol
         torch.cuda.empty_cache()
 
+    # Iterative reconstruction: one SIRT iteration on config 3 (1024 views
+    # of 1024^2 -> 1024^3) = forward projection + back-projection + element-wise steps, the
+    # normalisers precomputed; the forward projector timed alone as well (GUPS = voxel-view
+    # splats per second).  Measured projections = the analytic phantom's.
+    iterative = None
+    if world == 1 and not args.no_iterative:
+        from paper_1909_02724_b200 import SART, ifdk_fill, ifdk_forward_project
+
+        is_ = synth.config(3)
+        ig = Geometry.from_spec(is_)
+        ib = torch.empty((is_.Np, is_.Nv, is_.Nu), device=dev)
+        synth.project_gpu(is_.Nu, is_.Nv, is_.Du, is_.Dv, is_.D, is_.d, is_.theta,
+                          synth.default_ellipsoids(is_), 0, is_.Np, 0, is_.Nv,
+                          ib.data_ptr(), stream.cuda_stream)
+        st = SART(ig, ib)
+        ix = torch.empty((is_.Nz, is_.Ny, is_.Nx), device=dev)
+        ifdk_fill(ix, 0.0)
+        st.iterate(ix, 1)  # warm-up
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        st.iterate(ix, 2)
+        b.record()
+        b.synchronize()
+        it_ms = a.elapsed_time(b) / 2
+        a.record()
+        ifdk_forward_project(ig, ix, 0, ib)
+        b.record()
+        b.synchronize()
+        fp_ms = a.elapsed_time(b)
+        it_launches = last_launch_count()
+        iterative = {"workload": f"SIRT {is_.name}", "seconds_per_iteration": it_ms / 1e3,
+                     "fp_ms": fp_ms, "fp_gups": gups(is_, fp_ms / 1e3),
+                     "fp_kernel_launches": it_launches,
+                     "note": "one iteration = forward projection + ratio + back-projection + "
+                             "update over all 1024 views; normalisers R = M1, C = M^T 1 "
+                             "precomputed (DESIGN.md section 13)"}
+        del ib, ix, st
+        torch.cuda.empty_cache()
+
     if rank != 0:
         return
     cpu = None
@@ -584,6 +625,8 @@ def run_ours(args, spec, rank, world, local_rank):
         out["variants"] = variants
     if others:
         out["other_configs"] = others
+    if iterative:
+        out["iterative"] = iterative
     print(json.dumps(out), flush=True)
 
 

@@ -46,6 +46,7 @@ struct __align__(16) Box {
     int u_org, v_org, w, h;
 };
 
+template <bool SMALL_DV>
 __global__ void __launch_bounds__(kThreads, 2)
     fp_kernel(const __grid_constant__ FPParams p, const __grid_constant__ PTable pt)
 {
@@ -54,8 +55,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
     const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
     if (tile_i >= p.tiles_i) return;
-    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
-    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    // A warp's 32 columns are spread over the tile (stride 2 in i, 4 in j), not packed 8 x 4:
+    // neighbouring columns project onto the same detector pixel whenever the ray runs between
+    // them, and same-pixel lanes serialise a shared atomic; spread lanes collide only when the
+    // ray is within a narrow angle of their separation.
+    const int i = tile_i * kTI + (lane & 7) * 2 + (warp & 1);
+    const int j = tile_j * kTJ + (lane >> 3) * 4 + (warp >> 1);
     const bool active = i < p.Nx && j < p.Ny;
     const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
     const int kb = p.kb0 + (int)blockIdx.y * kKC;
@@ -153,30 +158,52 @@ __global__ void __launch_bounds__(kThreads, 2)
             int cur = (int)(floor_bits(fmaf((float)kv0, ti.dv, ti.fv0), &fr) - 0x4B000000u);
             float A = 0.f, B = 0.f;
             auto add_row = [&](int r, float sv) {  // Alg. alg:subpixel lines 4-5, transposed
-                if (sv != 0.f) {
-                    int* q = base + r * p.box_w;
-                    atomicAdd(q, __float2int_rn(sv * ws0));
-                    atomicAdd(q + 1, __float2int_rn(sv * ws1));
-                }
+                int* q = base + r * p.box_w;
+                atomicAdd(q, __float2int_rn(sv * ws0));
+                atomicAdd(q + 1, __float2int_rn(sv * ws1));
             };
+            if constexpr (SMALL_DV) {
+                // dv < 1: each slice stays on row cur or moves to cur + 1, so the walk is
+                // branch-free: the row add is predicated on the move, A/B shift by selects.
 #pragma unroll
-            for (int kk = 0; kk < kKC; ++kk) {
-                if (x[kk] == 0.f) continue;  // outside the slab (and empty voxels)
-                const int n = (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
-                if (n != cur) {  // the walk left row cur (n > cur)
-                    add_row(cur, A);
-                    if (n == cur + 1) {
-                        A = B;
-                    } else {
-                        add_row(cur + 1, B);
-                        A = 0.f;
+                for (int kk = 0; kk < kKC; ++kk) {
+                    const int n =
+                        (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+                    const bool adv = n != cur && kk >= kv0 && kk < kv1;
+                    int* q = base + cur * p.box_w;
+                    const int q0 = __float2int_rn(A * ws0), q1 = __float2int_rn(A * ws1);
+                    if (adv) {
+                        atomicAdd(q, q0);
+                        atomicAdd(q + 1, q1);
                     }
-                    B = 0.f;
-                    cur = n;
+                    A = adv ? B : A;
+                    B = adv ? 0.f : B;
+                    cur += adv ? 1 : 0;
+                    const float val = ti.W * x[kk];  // W_dis x (Alg. alg:bp line 8, transposed)
+                    A = fmaf(val, 1.f - fr, A);      // rows n, n+1 (line 6)
+                    B = fmaf(val, fr, B);
                 }
-                const float val = ti.W * x[kk];  // W_dis x (Alg. alg:bp line 8, transposed)
-                A = fmaf(val, 1.f - fr, A);      // rows n, n+1 (line 6)
-                B = fmaf(val, fr, B);
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < kKC; ++kk) {
+                    if (x[kk] == 0.f) continue;  // outside the slab (and empty voxels)
+                    const int n =
+                        (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+                    if (n != cur) {  // the walk left row cur (n > cur)
+                        if (A != 0.f) add_row(cur, A);
+                        if (n == cur + 1) {
+                            A = B;
+                        } else {
+                            if (B != 0.f) add_row(cur + 1, B);
+                            A = 0.f;
+                        }
+                        B = 0.f;
+                        cur = n;
+                    }
+                    const float val = ti.W * x[kk];
+                    A = fmaf(val, 1.f - fr, A);
+                    B = fmaf(val, fr, B);
+                }
             }
             add_row(cur, A);
             add_row(cur + 1, B);
@@ -218,7 +245,10 @@ ifdk_status launch_forward_project(const ifdk_geometry* g, const float* vol, int
     const double dv_min = g->D * g->Dz / (g->Dv * g->zmax);
     p.qfactor = (float)(256.0 * (1.0 / dv_min + 1.0) / (g->zmin * g->zmin));
     if (smem > 200 * 1024) return fail(IFDK_ERR_INVALID_ARGUMENT, "forward projector patch too large");
-    e = cudaFuncSetAttribute(fp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // dv/dk < 1 everywhere (all five configs): the branch-free walk
+    const bool small_dv = g->D * g->Dz / (g->Dv * g->zmin) < 0.999;
+    auto kern = small_dv ? fp_kernel<true> : fp_kernel<false>;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(fp)");
     dim3 grid((unsigned)(p.raster * tiles_j), (unsigned)n_chunks,
               (unsigned)((p.tiles_i + p.raster - 1) / p.raster));
@@ -228,7 +258,7 @@ ifdk_status launch_forward_project(const ifdk_geometry* g, const float* vol, int
         fill_ptable(g, s0 + t, n, pt);
         p.n_views = (int)n;
         p.proj = proj + (size_t)t * n_rows * g->Nu;
-        fp_kernel<<<grid, kThreads, smem, st>>>(p, pt);
+        kern<<<grid, kThreads, smem, st>>>(p, pt);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "fp_kernel launch");
         count_launch();
