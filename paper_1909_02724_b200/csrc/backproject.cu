@@ -333,18 +333,8 @@ __device__ __forceinline__ void accumulate_view_smem_x2(f2x (&acc)[KC / 2], uint
         const float eB = hi2(g) >= 0.f ? hi2(d12) : hi2(d01);
         const f2x val0 = fma2(fr, d01, h0);           // slices kk, kk+2 (line 6)
         const f2x val1 = fma2(g, pk2(eA, eB), h1);    // slices kk+1, kk+3
-        f2x& a0p = acc[kk / 2];
-        f2x& a1p = acc[kk / 2 + 1];
-        if (FULL) {
-            a0p = fma2(W2, val0, a0p);  // Alg. alg:bp line 10
-            a1p = fma2(W2, val1, a1p);
-        } else {
-            const f2x n0 = fma2(W2, val0, a0p), n1 = fma2(W2, val1, a1p);
-            a0p = pk2((kk >= kv0 && kk < kv1) ? lo2(n0) : lo2(a0p),
-                      (kk + 2 >= kv0 && kk + 2 < kv1) ? hi2(n0) : hi2(a0p));
-            a1p = pk2((kk + 1 >= kv0 && kk + 1 < kv1) ? lo2(n1) : lo2(a1p),
-                      (kk + 3 >= kv0 && kk + 3 < kv1) ? hi2(n1) : hi2(a1p));
-        }
+        acc[kk / 2] = fma2(W2, val0, acc[kk / 2]);  // Alg. alg:bp line 10
+        acc[kk / 2 + 1] = fma2(W2, val1, acc[kk / 2 + 1]);
     }
 }
 
@@ -713,6 +703,160 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
     }
 }
 
+// ---- RAW staging: the k-walk reads the TMA box itself (no pair rewrite) ---------------------
+// The PAIR walk on packed fp32x2 instructions (as accumulate_view_smem_x2) with the two taps of
+// each detector row read by two LDS.32 from the raw TMA box (row pitch BW floats, BW = 8 mod 32:
+// conflict-free for the 8 x 4 warp footprint) instead of one LDS.64 from a rewritten
+// (a, b - a) patch: the same shared-memory wavefronts per update in the walk (a warp's LDS.32
+// is one 128-byte wavefront, its LDS.64 two), and the rewrite -- 17 % of the kernel's shared
+// traffic, one extra pass over every box -- disappears.  b - a is formed in registers (FADD2),
+// so every value is bitwise that of the rewritten patch.
+__device__ __forceinline__ float lds32(uint32_t addr)
+{
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+template <int KC, int BW>
+__device__ __forceinline__ void accumulate_view_raw_x2(f2x (&acc)[KC / 2], uint32_t raw_base,
+                                                       uint32_t neg_magic, const ThreadInv& t,
+                                                       int u_org, int v_org)
+{
+    constexpr uint32_t S = BW * 4;
+    const uint32_t a0 = raw_base + (uint32_t)(((t.nv - v_org) * BW + (t.nu - u_org)) * 4) + neg_magic;
+    const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
+    const f2x du2 = pk2(t.du, t.du);
+    const f2x magic2 = pk2(8388608.0f, 8388608.0f), nmagic2 = pk2(-8388608.0f, -8388608.0f);
+    f2x fv02 = pk2(t.fv0, t.fv0);
+    f2x kpair = pk2(0.f, 2.f);
+    const f2x four2 = pk2(4.f, 4.f);
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+        if ((kk & 7) == 0) asm volatile("mov.b64 %0, %0;" : "+l"(fv02));
+        const f2x v = fma2(kpair, dv2, fv02);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(kpair) : "l"(four2));
+        const f2x tb = add2_rd(v, magic2);
+        const f2x fr = sub2(v, add2(tb, nmagic2));
+        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        f2x h[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const f2x a = pk2(lds32(adA + r * S), lds32(adB + r * S));
+            const f2x b = pk2(lds32(adA + r * S + 4), lds32(adB + r * S + 4));
+            h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
+        }
+        const f2x d01 = sub2(h[1], h[0]), d12 = sub2(h[2], h[1]);
+        const f2x g = add2(fr, dvm12);
+        const float eA = lo2(g) >= 0.f ? lo2(d12) : lo2(d01);
+        const float eB = hi2(g) >= 0.f ? hi2(d12) : hi2(d01);
+        const f2x val0 = fma2(fr, d01, h[0]);
+        const f2x val1 = fma2(g, pk2(eA, eB), h[1]);
+        acc[kk / 2] = fma2(W2, val0, acc[kk / 2]);  // Alg. alg:bp line 10
+        acc[kk / 2 + 1] = fma2(W2, val1, acc[kk / 2 + 1]);
+        // Pin the accumulation of each 8-slice group before the next group's loads: without
+        // it the compiler defers the FFMA2 chains to the end of the chunk and spills the
+        // pending values.
+        if ((kk & 7) == 4)
+            asm volatile("" : "+l"(acc[kk / 2 - 2]), "+l"(acc[kk / 2 - 1]), "+l"(acc[kk / 2]),
+                         "+l"(acc[kk / 2 + 1]));
+    }
+}
+
+constexpr int kRawBuf = 4;  // TMA boxes in flight / in use per CTA
+
+template <int KC, int BW>
+__global__ void __launch_bounds__(kThreads, 2)
+    bp_raw_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
+                  const __grid_constant__ PTable pt)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
+    const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
+    if (tile_i >= p.tiles_i) return;
+    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    const int ic = min(i, p.Nx - 1), jc = min(j, p.Ny - 1);
+    const int i_corner = (lane & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
+    const int j_corner = (lane & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
+    const int kb = p.kb0 + (int)blockIdx.y * KC;
+    if (kb < p.k0 || kb + KC > p.k0 + p.nk) __trap();  // whole chunks only (host)
+    const int kv0 = 0, kv1 = KC;
+
+    f2x acc[KC / 2];
+#pragma unroll
+    for (int q = 0; q < KC / 2; ++q) acc[q] = 0ull;
+    const int n = (int)p.n_views;
+
+    // shared memory: [raw box x kRawBuf | meta ring | mbarriers]; the box of view t is at
+    // raw + (t % kRawBuf) raw_bytes.  Whole chunks only (the host sends partial ones to the
+    // pair walk): every slice's rows lie inside the box.
+    unsigned char* const raw = smem;
+    Meta* const meta = reinterpret_cast<Meta*>(raw + kRawBuf * p.raw_bytes);
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
+    const uint32_t tx_bytes = (uint32_t)(BW * p.box_h * 4);
+    const CUtensorMap* const tmap_ptr = &tmap;
+    const PTable* const ptab = &pt;
+    const uint32_t raw0 = smem_u32(raw);
+
+    auto issue = [=](int t) {  // one thread: TMA of view t's box into raw buffer t % kRawBuf
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        if (!m.fast) __trap();  // the host sizes the box from a conservative bound
+        const int b = t % kRawBuf;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[b], tx_bytes);
+        tma_load_3d(raw + b * p.raw_bytes, tmap_ptr, &mbar[b], m.u_org, m.v_org - p.v0, t);
+    };
+    auto metas = [=](int t0) {  // all warps: boxes of views t0 .. t0+7
+        if (t0 + warp < n)
+            compute_meta1<KC, 2>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner, kb,
+                                 kv0, kv1);
+    };
+
+    if (tid == 0) {
+        for (int b = 0; b < kRawBuf; ++b) mbar_init(&mbar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    metas(0);
+    __syncthreads();
+    if (tid == 0)
+        for (int t = 0; t < kRawBuf && t < n; ++t) issue(t);
+
+    // first view after which the partial sums are flushed: s0 + t + 1 = 0 (mod vb); later
+    // flushes every vb views.  Derived from t (no loop-carried state next to the accumulators).
+    const int first_flush = (int)(p.vb - 1 - (p.s0 % p.vb + p.vb) % p.vb);
+    for (int t = 0; t < n; ++t) {
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        const int u_org = m.u_org, v_org = m.v_org;
+        // P_s straight from the constant bank (uniform per warp): no register copy of the 10
+        // doubles next to the 64 accumulators
+        // the column's coordinates are converted per view from laundered integers: hoisted out
+        // of the loop as doubles they would be spilled next to the 64 accumulators
+        int ic_ = ic, jc_ = jc, kb_ = kb;
+        asm volatile("" : "+r"(ic_), "+r"(jc_), "+r"(kb_));
+        const ThreadInv ti =
+            split(column_invariants(ptab->P[t], (double)ic_, (double)jc_, (double)kb_));
+        const int b = t % kRawBuf;
+        mbar_wait(&mbar[b], (uint32_t)((t / kRawBuf) & 1));
+        const uint32_t rb = raw0 + (uint32_t)(b * p.raw_bytes);
+        accumulate_view_raw_x2<KC, BW>(acc, rb, p.neg_magic, ti, u_org, v_org);
+        if ((t >= first_flush && (t - first_flush) % p.vb == 0) || t == n - 1) {
+            // recomputed here rather than kept live across the view loop
+            const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+            const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+            const bool ow = !p.accumulate && t <= first_flush;
+            if (fi < p.Nx && fj < p.Ny)
+                flush_x2<KC>(acc, p, fi, fj, kb, 0, KC, ow);
+        }
+        // boxes of views t+kRawBuf+1 .. +8 (the ring slots of views <= t+kRawBuf are in use)
+        if (((t + kRawBuf + 1) & 7) == 0) metas(t + kRawBuf + 1);
+        __syncthreads();  // buffer b read out by every warp
+        if (tid == 0 && t + kRawBuf < n) issue(t + kRawBuf);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -756,12 +900,15 @@ bool use_pair(const ifdk_geometry* g)
 }
 
 // Slices per floor of the k-walk when dv/dk < 1 for every z (all five configs): the PAIR
-// walk, issued on packed fp32x2 instructions (WALK 4, the default) or scalar (WALK 2; bitwise
-// the same values).  IFDK_BP_WALK=2|3|4 overrides: 3 selects the TRIPLE walk where
-// 0.5 <= dv/dk < 1 (configs 1-4), which needs 11 % less shared-memory traffic per update but
-// measured slower on B200 (config 4, 256 views: 1672 GUPS vs 1800 for scalar PAIR).
-// Otherwise 1 (IFDK_BP_PAIR=0 forces one floor per slice, with 32-slice chunks).
-constexpr int kDefaultPairWalk = 4;
+// walk.  Default (5): issued on packed fp32x2 instructions with the taps read straight from
+// the TMA box (bp_raw_kernel; partial chunks at slab ends take walk 4) -- measured on B200
+// (config 4 / 3, 256 views, same session): 1880 / 1879 GUPS vs 1780 / 1784 for walk 4 (x2
+// walk on the rewritten pair patch) and ~1800 for the scalar walk 2.  All three are bitwise
+// equal.  IFDK_BP_WALK=2|3|4|5 overrides: 3 selects the TRIPLE walk where 0.5 <= dv/dk < 1
+// (configs 1-4), which needs 11 % less shared-memory traffic per update but measured slower
+// (1672 GUPS vs 1800 for scalar PAIR).  Otherwise 1 (IFDK_BP_PAIR=0 forces one floor per
+// slice, with 32-slice chunks).
+constexpr int kDefaultPairWalk = 5;
 
 int choose_walk(const ifdk_geometry* g)
 {
@@ -770,7 +917,7 @@ int choose_walk(const ifdk_geometry* g)
     if (const char* e = std::getenv("IFDK_BP_WALK")) {
         const int v = std::atoi(e);
         const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
-        if (v == 2 || v == 4) w = v;
+        if (v == 2 || v == 4 || v == 5) w = v;
         if (v == 3 && dv_min >= 0.5001) w = 3;
     }
     return w;
@@ -821,40 +968,10 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     // Box of the staged patch from the conservative geometric bound.
     double wb, hb;
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
-    int box_w = ((int)std::ceil(wb) + 9 + 3) / 4 * 4;  // +3 for the 16-byte origin alignment
     p.pair = use_pair(g) ? 1 : 0;
-    p.walk = KC == 64 ? choose_walk(g) : (p.pair ? 2 : 1);
-    int box_h = (int)std::ceil(hb) + 6 + p.pair;
-    if (box_w < 8) box_w = 8;
-    int P2 = 0;
-    for (int c : {24, 40, 56, 72})
-        if (c >= box_w - 1) { P2 = c; break; }
-    bool tma = P2 != 0 && box_h <= 256 && (g->Nu % 4) == 0 &&
-               (reinterpret_cast<uintptr_t>(Q) % 16) == 0 && get_encode() != nullptr;
-    CUtensorMap map;
-    std::memset(&map, 0, sizeof(map));
-    size_t smem = 0;
-    if (tma) {
-        p.box_w = box_w;
-        p.box_h = box_h;
-        p.raw_bytes = (box_w * box_h * 4 + 127) / 128 * 128;
-        smem = 2 * (size_t)p.raw_bytes + 2 * sizeof(float2) * box_h * P2 + kMetaRing * sizeof(Meta) + 16;
-        cuuint64_t dims[3] = {(cuuint64_t)g->Nu, (cuuint64_t)n_rows, (cuuint64_t)n_views};
-        cuuint64_t strides[2] = {(cuuint64_t)g->Nu * 4, (cuuint64_t)g->Nu * 4 * n_rows};
-        cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
-        cuuint32_t estr[3] = {1, 1, 1};
-        CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)Q, dims,
-                                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) tma = false;
-    }
-    if (!tma) {
-        P2 = 24;
-        p.box_w = p.box_h = 0;
-        p.raw_bytes = 0;
-    }
-    p.neg_magic = 0u - 0x4B000000u * (uint32_t)(P2 * 8);
+    const int walk = KC == 64 ? choose_walk(g) : (p.pair ? 2 : 1);
+    const int box_h = (int)std::ceil(hb) + 6 + p.pair;
+    const int box_w0 = std::max(8, ((int)std::ceil(wb) + 9 + 3) / 4 * 4);  // +3: 16-B origin
     // Raster band of 16 tile columns: measured on B200 (config 4, one 256-view launch) DRAM
     // traffic 49 GB (algorithmic 39 GB) and L2 hit rate 95 %, vs 354 GB and 65 % for the
     // row-major raster, at the same speed (the kernel is shared-memory bound).
@@ -864,45 +981,111 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         const int r = std::atoi(e);
         p.raster = (r > 0 && r < p.tiles_i) ? r : p.tiles_i;
     }
-    dim3 grid((unsigned)(p.raster * tiles_j), (unsigned)n_chunks,
-              (unsigned)((p.tiles_i + p.raster - 1) / p.raster));
-    ifdk_status s;
-    if (p.walk == 3) {
-        switch (P2) {
-            case 24: s = launch_t<64, 24, 3>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<64, 40, 3>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<64, 56, 3>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<64, 72, 3>(p, map, pt, tma, grid, smem, st); break;
+    const bool tma_ok = box_h <= 256 && (g->Nu % 4) == 0 &&
+                        (reinterpret_cast<uintptr_t>(Q) % 16) == 0 && get_encode() != nullptr;
+
+    // One launch of chunks kb .. kb + nch KC - 1 with walk w (5 = RAW staging, full chunks only).
+    auto run = [&](int w, int kb, int nch) -> ifdk_status {
+        BPParams q = p;
+        q.kb0 = kb;
+        q.walk = w;
+        int box_w = box_w0, P2 = 0, BW = 0;
+        for (int c : {24, 40, 56, 72})
+            if (c >= box_w - 1) { P2 = c; break; }
+        if (w == 5) {
+            for (int c : {40, 72})  // row pitch = 8 mod 32 words: conflict-free LDS.32 taps
+                if (c >= box_w) { BW = c; break; }
+            box_w = BW;
         }
-    } else if (p.walk == 4) {
-        switch (P2) {
-            case 24: s = launch_t<64, 24, 4>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<64, 40, 4>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<64, 56, 4>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<64, 72, 4>(p, map, pt, tma, grid, smem, st); break;
+        bool tma = tma_ok && P2 != 0;
+        CUtensorMap map;
+        std::memset(&map, 0, sizeof(map));
+        size_t smem = 0;
+        if (tma) {
+            q.box_w = box_w;
+            q.box_h = box_h;
+            q.raw_bytes = (box_w * box_h * 4 + 127) / 128 * 128;
+            smem = BW ? kRawBuf * (size_t)q.raw_bytes + kMetaRing * sizeof(Meta) + 8 * kRawBuf
+                      : 2 * (size_t)q.raw_bytes + 2 * sizeof(float2) * box_h * P2 +
+                            kMetaRing * sizeof(Meta) + 16;
+            cuuint64_t dims[3] = {(cuuint64_t)g->Nu, (cuuint64_t)n_rows, (cuuint64_t)n_views};
+            cuuint64_t strides[2] = {(cuuint64_t)g->Nu * 4, (cuuint64_t)g->Nu * 4 * n_rows};
+            cuuint32_t box[3] = {(cuuint32_t)box_w, (cuuint32_t)box_h, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            CUresult r = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)Q, dims,
+                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) tma = false;
         }
-    } else if (p.walk == 2 && KC == 64) {
-        switch (P2) {
-            case 24: s = launch_t<64, 24, 2>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<64, 40, 2>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<64, 56, 2>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<64, 72, 2>(p, map, pt, tma, grid, smem, st); break;
+        if (!tma) {
+            P2 = 24;
+            BW = 0;
+            q.box_w = q.box_h = 0;
+            q.raw_bytes = 0;
         }
-    } else if (p.walk == 2) {
-        switch (P2) {
-            case 24: s = launch_t<32, 24, 2>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40, 2>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56, 2>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72, 2>(p, map, pt, tma, grid, smem, st); break;
+        q.neg_magic = 0u - 0x4B000000u * (uint32_t)(BW ? BW * 4 : P2 * 8);
+        dim3 grid((unsigned)(q.raster * tiles_j), (unsigned)nch,
+                  (unsigned)((q.tiles_i + q.raster - 1) / q.raster));
+        if (BW) {
+            auto k = BW == 40 ? bp_raw_kernel<64, 40> : bp_raw_kernel<64, 72>;
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp raw)");
+            k<<<grid, kThreads, smem, st>>>(q, map, pt);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "bp_raw_kernel launch");
+            count_launch();
+            return IFDK_OK;
         }
-    } else {
-        switch (P2) {
-            case 24: s = launch_t<32, 24, 1>(p, map, pt, tma, grid, smem, st); break;
-            case 40: s = launch_t<32, 40, 1>(p, map, pt, tma, grid, smem, st); break;
-            case 56: s = launch_t<32, 56, 1>(p, map, pt, tma, grid, smem, st); break;
-            default: s = launch_t<32, 72, 1>(p, map, pt, tma, grid, smem, st); break;
+        if (w == 5) w = 4;
+        if (w == 3) {
+            switch (P2) {
+                case 24: return launch_t<64, 24, 3>(q, map, pt, tma, grid, smem, st);
+                case 40: return launch_t<64, 40, 3>(q, map, pt, tma, grid, smem, st);
+                case 56: return launch_t<64, 56, 3>(q, map, pt, tma, grid, smem, st);
+                default: return launch_t<64, 72, 3>(q, map, pt, tma, grid, smem, st);
+            }
+        } else if (w == 4) {
+            switch (P2) {
+                case 24: return launch_t<64, 24, 4>(q, map, pt, tma, grid, smem, st);
+                case 40: return launch_t<64, 40, 4>(q, map, pt, tma, grid, smem, st);
+                case 56: return launch_t<64, 56, 4>(q, map, pt, tma, grid, smem, st);
+                default: return launch_t<64, 72, 4>(q, map, pt, tma, grid, smem, st);
+            }
+        } else if (w == 2 && KC == 64) {
+            switch (P2) {
+                case 24: return launch_t<64, 24, 2>(q, map, pt, tma, grid, smem, st);
+                case 40: return launch_t<64, 40, 2>(q, map, pt, tma, grid, smem, st);
+                case 56: return launch_t<64, 56, 2>(q, map, pt, tma, grid, smem, st);
+                default: return launch_t<64, 72, 2>(q, map, pt, tma, grid, smem, st);
+            }
+        } else if (w == 2) {
+            switch (P2) {
+                case 24: return launch_t<32, 24, 2>(q, map, pt, tma, grid, smem, st);
+                case 40: return launch_t<32, 40, 2>(q, map, pt, tma, grid, smem, st);
+                case 56: return launch_t<32, 56, 2>(q, map, pt, tma, grid, smem, st);
+                default: return launch_t<32, 72, 2>(q, map, pt, tma, grid, smem, st);
+            }
         }
-    }
+        switch (P2) {
+            case 24: return launch_t<32, 24, 1>(q, map, pt, tma, grid, smem, st);
+            case 40: return launch_t<32, 40, 1>(q, map, pt, tma, grid, smem, st);
+            case 56: return launch_t<32, 56, 1>(q, map, pt, tma, grid, smem, st);
+            default: return launch_t<32, 72, 1>(q, map, pt, tma, grid, smem, st);
+        }
+    };
+
+    if (walk != 5 || !tma_ok || box_w0 > 72) return run(walk, p.kb0, n_chunks);
+    // RAW staging runs the whole chunks; a partial chunk at either slab end (its masked slices
+    // would read rows outside the box) takes the x2 pair walk, bitwise the same values.
+    const bool head = (k0 % KC) != 0, tail = ((k0 + nk) % KC) != 0;
+    const int c0 = head ? 1 : 0, c1 = tail ? n_chunks - 1 : n_chunks;
+    ifdk_status s = IFDK_OK;
+    if (c1 > c0) s = run(5, p.kb0 + c0 * KC, c1 - c0);
+    if (s == IFDK_OK && head) s = run(4, p.kb0, 1);
+    if (s == IFDK_OK && tail && (n_chunks - 1 > 0 || !head)) s = run(4, p.kb0 + (n_chunks - 1) * KC, 1);
     return s;
 }
 

@@ -183,11 +183,12 @@ def test_bp_slab_split_is_bitwise_and_deterministic(torch_cuda):
             assert torch.equal(slab, full[a:b]), (cuts, a, b)
 
 
-@pytest.mark.parametrize("walk", ["2", "3"])
+@pytest.mark.parametrize("walk", ["2", "3", "5"])
 def test_bp_walk_variants(torch_cuda, monkeypatch, walk):
     """The default PAIR walk on packed fp32x2 instructions (WALK 4) gives bitwise the values of
-    the scalar PAIR walk (WALK 2: the same operations and roundings, element by element), on
-    whole chunks and on partial ones (slab cut inside a chunk); the TRIPLE walk (WALK 3)
+    the scalar PAIR walk (WALK 2: the same operations and roundings, element by element) and
+    of the RAW-staged walk (WALK 5: b - a formed in registers instead of in a rewritten patch),
+    on whole chunks and on partial ones (slab cut inside a chunk); the TRIPLE walk (WALK 3)
     matches the oracle."""
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_backproject
@@ -206,9 +207,9 @@ def test_bp_walk_variants(torch_cuda, monkeypatch, walk):
 
     x2 = run("4")
     other = run(walk)
-    if walk == "2":
+    if walk in ("2", "5"):  # scalar PAIR walk; RAW staging (taps straight from the TMA box)
         assert torch.equal(x2, other)
-        assert torch.equal(run("4", 77, 54), run("2", 77, 54))
+        assert torch.equal(run("4", 77, 54), run(walk, 77, 54))
     else:
         og = oracle.OracleGeometry(**spec.geometry_args())
         ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
