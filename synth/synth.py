@@ -207,14 +207,16 @@ def density(ell: np.ndarray, xyz: np.ndarray) -> np.ndarray:
     return out
 
 
-def phantom_volume(spec: ConfigSpec) -> np.ndarray:
-    """The phantom's density sampled at the voxel centres, [Nz][Ny][Nx] fp64: a seeded,
-    structured test volume for the forward projector (no method arithmetic)."""
-    k, j, i = np.meshgrid(np.arange(spec.Nz), np.arange(spec.Ny), np.arange(spec.Nx),
+def phantom_volume(spec: ConfigSpec, k0: int = 0, nk: int | None = None) -> np.ndarray:
+    """The phantom's density sampled at the voxel centres of slices k0..k0+nk-1,
+    [nk][Ny][Nx] fp64: a structured test volume for the forward projector (no method
+    arithmetic)."""
+    nk = spec.Nz - k0 if nk is None else nk
+    k, j, i = np.meshgrid(np.arange(k0, k0 + nk), np.arange(spec.Ny), np.arange(spec.Nx),
                           indexing="ij")
     X, Y, Z = voxel_world(spec, i.ravel(), j.ravel(), k.ravel())
     rho = density(default_ellipsoids(spec), np.stack([X, Y, Z], axis=1))
-    return rho.reshape(spec.Nz, spec.Ny, spec.Nx)
+    return rho.reshape(nk, spec.Ny, spec.Nx)
 
 
 def add_noise(E: np.ndarray, sigma: float, seed: int = 1234, base: int = 0) -> np.ndarray:
