@@ -42,6 +42,20 @@ struct FPParams {
     float qfactor;     // bound on a patch pixel's sum per unit |x|: 256 (1/dv_min + 1) / zmin^2
 };
 
+__device__ __forceinline__ uint32_t smem_u32_fp(const void* q)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(q));
+}
+
+// shared-memory integer add, predicated in the instruction (no branch around it)
+__device__ __forceinline__ void red_add_if(uint32_t addr, int v, uint32_t pred)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p red.shared.add.s32 [%0], %1;\n}" ::"r"(addr),
+        "r"(v), "r"(pred)
+        : "memory");
+}
+
 struct __align__(16) Box {
     int u_org, v_org, w, h;
 };
@@ -65,6 +79,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
     const int kb = p.kb0 + (int)blockIdx.y * kKC;
     const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, kKC);
+    const bool full = kv0 == 0 && kv1 == kKC;
     const int cap = p.box_w * p.box_h;
     Box* const box = reinterpret_cast<Box*>(fsm);  // four slots (t & 3)
     float* const wmax = fsm + 4 * sizeof(Box) / sizeof(float);  // 8 per-warp maxima
@@ -163,25 +178,49 @@ __global__ void __launch_bounds__(kThreads, 2)
                 atomicAdd(q + 1, __float2int_rn(sv * ws1));
             };
             if constexpr (SMALL_DV) {
-                // dv < 1: each slice stays on row cur or moves to cur + 1, so the walk is
-                // branch-free: the row add is predicated on the move, A/B shift by selects.
+                if (full) {
+                    // dv < 1, whole chunk: each slice stays on row cur or moves to cur + 1.
+                    // One branch around the two integer reds at a running row address, the
+                    // A/B shift by selects, no slab masks (measured: 690 vs 655 GUPS; reds
+                    // predicated inside the instruction were compiled to two branches, 560).
+                    uint32_t rowp = smem_u32_fp(base + cur * p.box_w);
+                    const uint32_t pitch = (uint32_t)p.box_w * 4u;
 #pragma unroll
-                for (int kk = 0; kk < kKC; ++kk) {
-                    const int n =
-                        (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
-                    const bool adv = n != cur && kk >= kv0 && kk < kv1;
-                    int* q = base + cur * p.box_w;
-                    const int q0 = __float2int_rn(A * ws0), q1 = __float2int_rn(A * ws1);
-                    if (adv) {
-                        atomicAdd(q, q0);
-                        atomicAdd(q + 1, q1);
+                    for (int kk = 0; kk < kKC; ++kk) {
+                        const int n =
+                            (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+                        const uint32_t adv = n != cur ? 1u : 0u;
+                        if (adv) {
+                            red_add_if(rowp, __float2int_rn(A * ws0), 1u);
+                            red_add_if(rowp + 4, __float2int_rn(A * ws1), 1u);
+                        }
+                        A = adv ? B : A;
+                        B = adv ? 0.f : B;
+                        rowp += adv * pitch;
+                        cur = n;
+                        const float val = ti.W * x[kk];  // W_dis x (Alg. alg:bp line 8, transposed)
+                        A = fmaf(val, 1.f - fr, A);      // rows n, n+1 (line 6)
+                        B = fmaf(val, fr, B);
                     }
-                    A = adv ? B : A;
-                    B = adv ? 0.f : B;
-                    cur += adv ? 1 : 0;
-                    const float val = ti.W * x[kk];  // W_dis x (Alg. alg:bp line 8, transposed)
-                    A = fmaf(val, 1.f - fr, A);      // rows n, n+1 (line 6)
-                    B = fmaf(val, fr, B);
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < kKC; ++kk) {
+                        const int n =
+                            (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+                        const bool adv = n != cur && kk >= kv0 && kk < kv1;
+                        int* q = base + cur * p.box_w;
+                        const int q0 = __float2int_rn(A * ws0), q1 = __float2int_rn(A * ws1);
+                        if (adv) {
+                            atomicAdd(q, q0);
+                            atomicAdd(q + 1, q1);
+                        }
+                        A = adv ? B : A;
+                        B = adv ? 0.f : B;
+                        cur += adv ? 1 : 0;
+                        const float val = ti.W * x[kk];
+                        A = fmaf(val, 1.f - fr, A);
+                        B = fmaf(val, fr, B);
+                    }
                 }
             } else {
 #pragma unroll
