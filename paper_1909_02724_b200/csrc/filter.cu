@@ -187,43 +187,96 @@ constexpr int L = 4096, T = 256;
 
 __device__ __forceinline__ int padx(int q) { return q + (q >> 4); }  // 1 pad word per 16
 
-__device__ __forceinline__ float2 cmulf(float2 a, float2 b)
+// Complex values ride in one 64-bit register pair (re, im) and every butterfly is a Blackwell
+// packed fp32x2 instruction: a complex add is one FADD2, a multiplication by -i is free (the
+// consumer's operand takes the halves swapped and one negated, .LO_HI / .N modifiers), a
+// complex multiply is FMUL2 + FFMA2 with broadcast operands -- half the FP32 instructions of
+// the scalar butterflies.
+using cx = unsigned long long;
+
+__device__ __forceinline__ cx mk(float re, float im)
 {
-    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+    cx r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(re), "f"(im));
+    return r;
+}
+__device__ __forceinline__ float re_(cx v)
+{
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return a;
+}
+__device__ __forceinline__ float im_(cx v)
+{
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    return b;
+}
+__device__ __forceinline__ cx cadd(cx a, cx b)
+{
+    cx r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ cx csub(cx a, cx b)
+{
+    cx r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ cx cmul2(cx a, cx b)  // element-wise
+{
+    cx r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ cx cfma2(cx a, cx b, cx c)  // element-wise a b + c
+{
+    cx r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ cx negi(cx v) { return mk(im_(v), -re_(v)); }  // -i v
+
+// a b = a.re (b.re, b.im) + a.im (-b.im, b.re)
+__device__ __forceinline__ cx cmulf(cx a, cx b)
+{
+    const float ar = re_(a), ai = im_(a);
+    return cfma2(mk(ai, ai), mk(-im_(b), re_(b)), cmul2(mk(ar, ar), b));
 }
 
-__device__ __forceinline__ void dft4(float2& a, float2& b, float2& c, float2& d)
+__device__ __forceinline__ void dft4(cx& a, cx& b, cx& c, cx& d)
 {
-    const float2 t0 = make_float2(a.x + c.x, a.y + c.y), t1 = make_float2(a.x - c.x, a.y - c.y);
-    const float2 t2 = make_float2(b.x + d.x, b.y + d.y);
-    const float2 t3 = make_float2(b.y - d.y, d.x - b.x);  // -i (b - d)
-    a = make_float2(t0.x + t2.x, t0.y + t2.y);
-    c = make_float2(t0.x - t2.x, t0.y - t2.y);
-    b = make_float2(t1.x + t3.x, t1.y + t3.y);
-    d = make_float2(t1.x - t3.x, t1.y - t3.y);
+    const cx t0 = cadd(a, c), t1 = csub(a, c);
+    const cx t2 = cadd(b, d);
+    const cx t3 = negi(csub(b, d));  // -i (b - d)
+    a = cadd(t0, t2);
+    c = csub(t0, t2);
+    b = cadd(t1, t3);
+    d = csub(t1, t3);
 }
 
 // 16-point forward DFT in place: n = 4 n1 + n2, k = k1 + 4 k2 (two radix-4 stages).
-__device__ __forceinline__ void dft16(float2 (&u)[16])
+__device__ __forceinline__ void dft16(cx (&u)[16])
 {
     constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f,
                     C2 = 0.70710678118654752f;
 #pragma unroll
     for (int n2 = 0; n2 < 4; ++n2) dft4(u[n2], u[4 + n2], u[8 + n2], u[12 + n2]);
     // A[n2][k1] (at u[4 k1 + n2]) *= W16^(n2 k1)
-    u[5] = cmulf(u[5], make_float2(C1, -S1));    // W^1
-    u[6] = cmulf(u[6], make_float2(C2, -C2));    // W^2
-    u[7] = cmulf(u[7], make_float2(S1, -C1));    // W^3
-    u[9] = cmulf(u[9], make_float2(C2, -C2));    // W^2
-    u[10] = make_float2(u[10].y, -u[10].x);      // W^4 = -i
-    u[11] = cmulf(u[11], make_float2(-C2, -C2)); // W^6
-    u[13] = cmulf(u[13], make_float2(S1, -C1));  // W^3
-    u[14] = cmulf(u[14], make_float2(-C2, -C2)); // W^6
-    u[15] = cmulf(u[15], make_float2(-C1, S1));  // W^9
+    u[5] = cmulf(u[5], mk(C1, -S1));    // W^1
+    u[6] = cmulf(u[6], mk(C2, -C2));    // W^2
+    u[7] = cmulf(u[7], mk(S1, -C1));    // W^3
+    u[9] = cmulf(u[9], mk(C2, -C2));    // W^2
+    u[10] = negi(u[10]);                // W^4 = -i
+    u[11] = cmulf(u[11], mk(-C2, -C2)); // W^6
+    u[13] = cmulf(u[13], mk(S1, -C1));  // W^3
+    u[14] = cmulf(u[14], mk(-C2, -C2)); // W^6
+    u[15] = cmulf(u[15], mk(-C1, S1));  // W^9
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) dft4(u[4 * k1], u[4 * k1 + 1], u[4 * k1 + 2], u[4 * k1 + 3]);
     // X[k1 + 4 k2] sits at u[4 k1 + k2]: transpose by renaming
-    float2 v[16];
+    cx v[16];
 #pragma unroll
     for (int m = 0; m < 16; ++m) v[m] = u[4 * (m & 3) + (m >> 2)];
 #pragma unroll
@@ -231,23 +284,46 @@ __device__ __forceinline__ void dft16(float2 (&u)[16])
 }
 
 // Twiddle w^e, w = exp(-2 pi i / 4096), from two small tables: w^(16 a) and w^b.
-__device__ __forceinline__ float2 twiddle(const float2* twA, const float2* twB, int e)
+__device__ __forceinline__ cx twiddle(const cx* twA, const cx* twB, int e)
 {
-    const float2 a = twA[e >> 4];
+    const cx a = twA[e >> 4];
     const int b = e & 15;
     return b ? cmulf(a, twB[b]) : a;
+}
+
+// w^(j e) for j = 1 .. 15 from four table twiddles w^e, w^2e, w^4e, w^8e: every power is a
+// product of at most four of them (<= 3 extra roundings), 8 table reads instead of 30.
+__device__ __forceinline__ void twiddle_powers(cx (&w)[16], const cx* twA, const cx* twB, int e)
+{
+    w[1] = twiddle(twA, twB, e);
+    w[2] = twiddle(twA, twB, 2 * e);
+    w[4] = twiddle(twA, twB, 4 * e);
+    w[8] = twiddle(twA, twB, 8 * e);
+    w[3] = cmulf(w[2], w[1]);
+    w[5] = cmulf(w[4], w[1]);
+    w[6] = cmulf(w[4], w[2]);
+    w[7] = cmulf(w[6], w[1]);
+    w[9] = cmulf(w[8], w[1]);
+    w[10] = cmulf(w[8], w[2]);
+    w[11] = cmulf(w[10], w[1]);
+    w[12] = cmulf(w[8], w[4]);
+    w[13] = cmulf(w[12], w[1]);
+    w[14] = cmulf(w[12], w[2]);
+    w[15] = cmulf(w[14], w[1]);
 }
 
 // One Stockham radix-16 pass of span P on the values u (= x[i + 256 j]) of thread i; writes
 // the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
 template <int P>
-__device__ __forceinline__ void pass_out(float2 (&u)[16], float2* buf, const float2* twA,
-                                         const float2* twB, int i)
+__device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* twA, const cx* twB,
+                                         int i)
 {
     const int k = i & (P - 1);
     if (P > 1) {
+        cx w[16];
+        twiddle_powers(w, twA, twB, k * (256 / P));
 #pragma unroll
-        for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], twiddle(twA, twB, j * k * (256 / P)));
+        for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
     }
     dft16(u);
     const int base = (i - k) * 16 + k;
@@ -255,7 +331,7 @@ __device__ __forceinline__ void pass_out(float2 (&u)[16], float2* buf, const flo
     for (int m = 0; m < 16; ++m) buf[padx(base + m * P)] = u[m];
 }
 
-__device__ __forceinline__ void load_in(float2 (&u)[16], const float2* buf, int i)
+__device__ __forceinline__ void load_in(cx (&u)[16], const cx* buf, int i)
 {
 #pragma unroll
     for (int j = 0; j < 16; ++j) u[j] = buf[padx(i + j * T)];
@@ -264,8 +340,8 @@ __device__ __forceinline__ void load_in(float2 (&u)[16], const float2* buf, int 
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
 // X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
 // barrier: a buffer is rewritten only after the barrier that follows its last read.
-__device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf0, float2* buf1,
-                                        const float2* twA, const float2* twB, int i)
+__device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const cx* twA,
+                                        const cx* twB, int i)
 {
     pass_out<1>(u, buf0, twA, twB, i);
     __syncthreads();
@@ -273,9 +349,11 @@ __device__ __forceinline__ void fft4096(float2 (&u)[16], float2* buf0, float2* b
     pass_out<16>(u, buf1, twA, twB, i);
     __syncthreads();
     load_in(u, buf1, i);
-    const int k = i;  // span 256: k = i, outputs at i + 256 m stay in this thread
+    // span 256: k = i, outputs at i + 256 m stay in this thread
+    cx w[16];
+    twiddle_powers(w, twA, twB, i);
 #pragma unroll
-    for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], twiddle(twA, twB, j * k));
+    for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
     dft16(u);
 }
 
@@ -295,15 +373,15 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
 {
     using namespace f4k;
     extern __shared__ __align__(16) unsigned char fsm[];
-    float2* const buf = reinterpret_cast<float2*>(fsm);  // 2 x (L + L/16) (padded)
-    float2* const bufB = buf + (L + L / 16);
-    float2* const twA = bufB + (L + L / 16);               // 256
-    float2* const twB = twA + 256;                          // 16
+    cx* const buf = reinterpret_cast<cx*>(fsm);  // 2 x (L + L/16) (padded)
+    cx* const bufB = buf + (L + L / 16);
+    cx* const twA = bufB + (L + L / 16);          // 256
+    cx* const twB = twA + 256;                    // 16
     float* const Hs = reinterpret_cast<float*>(twB + 16);   // L/2 + 1 (2052 slots)
     float* const stage = Hs + 2052;                         // 2 rows
     const int i = threadIdx.x;
-    twA[i] = twA_g[i];
-    if (i < 16) twB[i] = twB_g[i];
+    twA[i] = reinterpret_cast<const cx*>(twA_g)[i];
+    if (i < 16) twB[i] = reinterpret_cast<const cx*>(twB_g)[i];
     for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
     const long n_pairs = (p.n_rows_total + 1) / 2;
     auto prefetch = [&](long pr) {
@@ -335,12 +413,12 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();
         }
-        float2 u[16];
+        cx u[16];
         // Alg. alg:filter line 2: E~ = E . F_cos (reading c-A5), rows A | B packed, zero padded.
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int n = i + j * T;
-            float2 x = make_float2(0.f, 0.f);
+            float2 x = make_float2(0.f, 0.f);  // (row A, row B)
             if (j < 8 && n < p.Nu) {
                 const float uh = ((float)n - p.cu) * p.Du;
                 // F_cos = D / sqrt(D^2 + uh^2 + vh^2); rsqrtf's <= 2 ulp error is far below the
@@ -348,7 +426,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
                 x.x = (ASYNC ? eA[n] : __ldg(eA + n)) * (p.D * rsqrtf(fmaf(uh, uh, dA)));
                 if (hasB) x.y = (ASYNC ? eB[n] : __ldg(eB + n)) * (p.D * rsqrtf(fmaf(uh, uh, dB)));
             }
-            u[j] = x;
+            u[j] = mk(x.x, x.y);
         }
         __syncthreads();  // staging read and buffers free: fetch the next pair meanwhile
         prefetch(pr + gridDim.x);
@@ -358,7 +436,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
         for (int m = 0; m < 16; ++m) {
             const int f = i + m * T;
             const float h = Hs[f <= L / 2 ? f : L - f];
-            u[m] = make_float2(u[m].x * h, -u[m].y * h);
+            u[m] = cmul2(u[m], mk(h, -h));
         }
         fft4096(u, buf, bufB, twA, twB, i);  // buf's last reader was before bufB's barrier
         // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1 (to every destination
@@ -371,8 +449,8 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             for (int m = 0; m < 8; ++m) {
                 const int n = i + m * T;
                 if (n < p.Nu) {
-                    if (qA) qA[n] = u[m].x;
-                    if (qB) qB[n] = -u[m].y;
+                    if (qA) qA[n] = re_(u[m]);
+                    if (qB) qB[n] = -im_(u[m]);
                 }
             }
         }
