@@ -132,6 +132,15 @@ def ncu_traffic(config: int):
     return None
 
 
+def ncu_field(config: int, key: str):
+    p = os.path.join(ROOT, "profiles", "ncu_bp_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            e = json.load(f).get(str(config))
+        return e.get(key) if e else None
+    return None
+
+
 def smem_probe():
     """Measured shared-memory gather bandwidth (bytes/s) from libifdk_probe.so, or None."""
     import ctypes
@@ -213,7 +222,11 @@ def run_reference(args, spec, rank, world):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (analytic Shepp-Logan projections, seeded)",
-        "config": {"workload": spec.name, "config_id": args.config},
+        "config": {"workload": spec.name, "config_id": args.config,
+                   "Np": spec.Np, "Nu": spec.Nu, "Nv": spec.Nv,
+                   "volume": [spec.Nx, spec.Ny, spec.Nz],
+                   "parallelism": "host cores (fp64 oracle, OpenMP over voxels)",
+                   "l2": "n/a (CPU); a bounded sample of the workload per step"},
         "cpu_baseline": {"value": value, "unit": "GUPS", "cores": cores, "kind": "oracle",
                          "sample": desc},
         "e2e": {"value": value, "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -365,6 +378,19 @@ def run_ours(args, spec, rank, world, local_rank):
                     "unit": "GB/s", "frac": bp_hbm_bytes / bp_s / 1e9 / hbm_peak,
                     "kernel": "bp_raw_kernel (4 B per filtered pixel + 8 B per voxel per launch)",
                     "peak_basis": "MEASURED_PEAKS.json hbm_gbs"}
+    # BP against the issue roofline: SASS instructions per update from the committed ncu
+    # capture (profiles/ncu_bp_traffic.json "inst_per_update") x updates/s, against
+    # 148 SMs x 4 schedulers x 32 lanes x the SM clock.
+    roofline_issue = None
+    ipu = ncu_field(args.config, "inst_per_update")
+    if ipu:
+        sm_hz = float(measured_peaks().get("sm_max_mhz", 1965.0)) * 1e6
+        peak_ti = 148 * 4 * 32 * sm_hz / 1e12  # thread-instructions per second, x1e12
+        ach_ti = ipu * upd_per_launch / bp_s / 1e12
+        roofline_issue = {"bound": "issue", "achieved": ach_ti, "peak": peak_ti,
+                          "unit": "Tinst/s (thread)", "frac": ach_ti / peak_ti,
+                          "inst_per_update": ipu,
+                          "kernel": "bp_raw_kernel", "peak_basis": "148 SM x 4 x 32 x sm_max_mhz"}
     filt = None
     if filter_events:
         fdur = sum(a.elapsed_time(b) for a, b, _ in filter_events) / len(filter_events) / 1e3
@@ -613,6 +639,7 @@ def run_ours(args, spec, rank, world, local_rank):
                      "kernel": "bp_raw_kernel (16 algorithmic B/update of bilinear taps)",
                      "peak_basis": peak_basis},
         "roofline_hbm": roofline_hbm,
+        "roofline_issue": roofline_issue,
         "filter_roofline": filt,
         "clocks": clk,
         "e2e": e2e,
