@@ -12,9 +12,12 @@
 //  * The detector patch the tile x chunk projects onto (its extent is bounded from the
 //    tile corners: u, v are linear-fractional, so extremes sit at corners) is staged per
 //    view by TMA (cp.async.bulk.tensor, OOB zero fill = the per-tap zero border, reading
-//    c-A9) into a double-buffered raw box, then rewritten once into (Q[r][c], Q[r][c+1] -
-//    Q[r][c]) pairs so that each detector row costs one LDS.64 and one FMA per update.
-//    TMA for view t+3 is in flight while view t is accumulated.
+//    c-A9).  Default (bp_raw_kernel, walk 5): four boxes in flight per CTA and the walk
+//    reads both taps of a row straight from the box (two LDS.32, row pitch 8 mod 32 words);
+//    the PAIR walk (two slices per floor) runs on packed fp32x2 instructions.  Variants
+//    (bp_kernel, walks 1-4): a double-buffered box rewritten once into (Q[r][c], Q[r][c+1] -
+//    Q[r][c]) pairs (one LDS.64 per row), scalar or fp32x2 walks; walk 4 also serves the
+//    partial chunks at slab ends for walk 5.  All PAIR variants are bitwise equal.
 //  * P_s lives in constant memory: each launch carries the fp64 rows of its <= 256 views in
 //    a __grid_constant__ kernel parameter (param space = the constant bank), so no
 //    per-launch device allocation or host-to-device copy is needed.  Longer view ranges are
