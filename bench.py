@@ -132,6 +132,17 @@ def ncu_traffic(config: int):
     return None
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def ncu_field(config: int, key: str):
     p = os.path.join(ROOT, "profiles", "ncu_bp_traffic.json")
     if os.path.exists(p):
@@ -228,7 +239,7 @@ def run_reference(args, spec, rank, world):
                    "parallelism": "host cores (fp64 oracle, OpenMP over voxels)",
                    "l2": "n/a (CPU); a bounded sample of the workload per step"},
         "cpu_baseline": {"value": value, "unit": "GUPS", "cores": cores, "kind": "oracle",
-                         "sample": desc},
+                         "sample": desc, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -606,7 +617,14 @@ def run_ours(args, spec, rank, world, local_rank):
         oracle.build()
         v, s, desc = oracle_sample(spec, 32, 1 << 25)  # ~10-20 s on the box's 16 cores
         cpu = {"value": v, "unit": "GUPS", "cores": oracle.num_threads(), "kind": "oracle",
-               "sample": desc, "seconds": s}
+               "sample": desc, "seconds": s, "cpu_model": cpu_model()}
+        # config 1 (the case the oracle finishes in seconds) in full: filter + back-projection
+        c1 = synth.config(1)
+        E1 = synth.project(c1.Nu, c1.Nv, c1.Du, c1.Dv, c1.D, c1.d, c1.theta,
+                           synth.default_ellipsoids(c1), 0, c1.Np)
+        t1 = time.perf_counter()
+        oracle.reconstruct(oracle.OracleGeometry(**c1.geometry_args()), E1)
+        cpu["config1_full_seconds"] = time.perf_counter() - t1
     value = gups(spec, ms / 1e3)
     out = {
         "metric": "fdk_gups",
