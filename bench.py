@@ -358,14 +358,17 @@ def run_ours(args, spec, rank, world, local_rank):
     for _ in range(args.steps):
         launches += step(True)
         for k, v in timings.items():
-            stage[k] = stage.get(k, 0.0) + v
+            if isinstance(v, (int, float)):
+                stage[k] = stage.get(k, 0.0) + v
+            else:  # labels (e.g. which exchange ran)
+                stage[k] = v
     t_end.record()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
     ms = _max_over_ranks(t_start.elapsed_time(t_end) / args.steps, world, dev)
-    stage = {k: v / args.steps for k, v in stage.items()}
+    stage = {k: (v / args.steps if isinstance(v, (int, float)) else v) for k, v in stage.items()}
 
     # Dominant kernel: the back-projection; algorithmic smem bytes / its launch duration.
     if bp_events:
@@ -643,8 +646,9 @@ def run_ours(args, spec, rank, world, local_rank):
         "config": {"workload": spec.name, "config_id": args.config,
                    "Np": spec.Np, "Nu": spec.Nu, "Nv": spec.Nv,
                    "volume": [spec.Nx, spec.Ny, spec.Nz],
-                   "parallelism": f"k-slab x{world} (pipelined 128-view rounds, NCCL band "
-                                  "all-to-all)" if use_kslab else "single GPU",
+                   "parallelism": (f"k-slab x{world} (pipelined 128-view rounds, band exchange: "
+                                  f"{stage.get('exchange', 'none')})") if use_kslab
+                                 else "single GPU",
                    "l2": f"projections ({4 * spec.Np * spec.Nu * spec.Nv / 2**30:.0f} GiB) and "
                          f"volume ({4 * spec.Nx * spec.Ny * spec.Nz / 2**30:.0f} GiB) far larger "
                          "than the 126 MB L2; no flush"},
