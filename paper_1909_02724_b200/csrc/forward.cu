@@ -138,18 +138,27 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
     // add the patch of view t to the projection (non-zero, on-detector, in-band taps) and
     // zero what was read, so the buffer is clean for view t+2
+    const int r0 = tid / p.box_w, c0 = tid - r0 * p.box_w;
+    const int dr = kThreads / p.box_w, dc = kThreads - dr * p.box_w;
     auto flush = [&](int t) {
         const Box b = box[t & 3];
         int* const pa = patch0 + (t & 1) * cap;
         float* const pv = p.proj + (long)t * p.n_rows * p.Nu;
+        // (r, c) of element e = tid + kThreads q stepped incrementally (no division per element)
+        int r = r0, c = c0;
         for (int e = tid; e < b.h * p.box_w; e += kThreads) {
-            const int r = e / p.box_w, c = e - r * p.box_w;
             const int q = pa[e];
             pa[e] = 0;
             const int col = b.u_org + c, row = b.v_org + r;
             if (q != 0 && c < b.w && col >= 0 && col < p.Nu && row >= p.v0 &&
                 row < p.v0 + p.n_rows)
                 atomicAdd(pv + (long)(row - p.v0) * p.Nu + col, (float)q * inv_scale);
+            c += dc;
+            r += dr;
+            if (c >= p.box_w) {
+                c -= p.box_w;
+                ++r;
+            }
         }
     };
 
