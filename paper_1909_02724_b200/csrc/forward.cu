@@ -194,23 +194,30 @@ __global__ void __launch_bounds__(kThreads, 2)
                     // predicated inside the instruction were compiled to two branches, 560).
                     uint32_t rowp = smem_u32_fp(base + cur * p.box_w);
                     const uint32_t pitch = (uint32_t)p.box_w * 4u;
+                    // W folded into the column weights; the walk keeps S = the x sum of the
+                    // current row window and Bx = its fr-weighted part, so row cur holds
+                    // S - Bx and row cur + 1 holds Bx (one FADD + one FFMA per slice).
+                    const float wW0 = ws0 * ti.W, wW1 = ws1 * ti.W;
+                    float S = 0.f, Bx = 0.f;
 #pragma unroll
                     for (int kk = 0; kk < kKC; ++kk) {
                         const int n =
                             (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
                         const uint32_t adv = n != cur ? 1u : 0u;
                         if (adv) {
-                            red_add_if(rowp, __float2int_rn(A * ws0), 1u);
-                            red_add_if(rowp + 4, __float2int_rn(A * ws1), 1u);
+                            const float a = S - Bx;
+                            red_add_if(rowp, __float2int_rn(a * wW0), 1u);
+                            red_add_if(rowp + 4, __float2int_rn(a * wW1), 1u);
                         }
-                        A = adv ? B : A;
-                        B = adv ? 0.f : B;
+                        S = adv ? Bx : S;
+                        Bx = adv ? 0.f : Bx;
                         rowp += adv * pitch;
                         cur = n;
-                        const float val = ti.W * x[kk];  // W_dis x (Alg. alg:bp line 8, transposed)
-                        A = fmaf(val, 1.f - fr, A);      // rows n, n+1 (line 6)
-                        B = fmaf(val, fr, B);
+                        S += x[kk];                 // W_dis x (Alg. alg:bp line 8, transposed)
+                        Bx = fmaf(x[kk], fr, Bx);   // rows n, n+1 (line 6)
                     }
+                    A = (S - Bx) * ti.W;
+                    B = Bx * ti.W;
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < kKC; ++kk) {
