@@ -283,22 +283,18 @@ __device__ __forceinline__ void dft16(cx (&u)[16])
     for (int m = 0; m < 16; ++m) u[m] = v[m];
 }
 
-// Twiddle w^e, w = exp(-2 pi i / 4096), from two small tables: w^(16 a) and w^b.
-__device__ __forceinline__ cx twiddle(const cx* twA, const cx* twB, int e)
-{
-    const cx a = twA[e >> 4];
-    const int b = e & 15;
-    return b ? cmulf(a, twB[b]) : a;
-}
+// Twiddle tables (host fp64, rounded once): TL[q][i] = w^(2^q i) for the span-256 pass
+// (thread i) and T16[q][k] = w^(16 2^q k) for the span-16 pass (k = i mod 16), each read with
+// consecutive indices across a warp (no bank conflicts).  w^(j e) for j = 1 .. 15 is then a
+// product of at most four table values (<= 3 roundings).
+constexpr int kTwL = 0, kTw16 = 4 * 256, kTwEntries = 4 * 256 + 4 * 16;
 
-// w^(j e) for j = 1 .. 15 from four table twiddles w^e, w^2e, w^4e, w^8e: every power is a
-// product of at most four of them (<= 3 extra roundings), 8 table reads instead of 30.
-__device__ __forceinline__ void twiddle_powers(cx (&w)[16], const cx* twA, const cx* twB, int e)
+__device__ __forceinline__ void twiddle_powers(cx (&w)[16], const cx* tw, int stride, int idx)
 {
-    w[1] = twiddle(twA, twB, e);
-    w[2] = twiddle(twA, twB, 2 * e);
-    w[4] = twiddle(twA, twB, 4 * e);
-    w[8] = twiddle(twA, twB, 8 * e);
+    w[1] = tw[idx];
+    w[2] = tw[stride + idx];
+    w[4] = tw[2 * stride + idx];
+    w[8] = tw[3 * stride + idx];
     w[3] = cmulf(w[2], w[1]);
     w[5] = cmulf(w[4], w[1]);
     w[6] = cmulf(w[4], w[2]);
@@ -315,13 +311,13 @@ __device__ __forceinline__ void twiddle_powers(cx (&w)[16], const cx* twA, const
 // One Stockham radix-16 pass of span P on the values u (= x[i + 256 j]) of thread i; writes
 // the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
 template <int P>
-__device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* twA, const cx* twB,
-                                         int i)
+__device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* tw, int i)
 {
+    static_assert(P == 1 || P == 16, "span-1 and span-16 passes");
     const int k = i & (P - 1);
     if (P > 1) {
         cx w[16];
-        twiddle_powers(w, twA, twB, k * (256 / P));
+        twiddle_powers(w, tw + kTw16, 16, k);
 #pragma unroll
         for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
     }
@@ -340,18 +336,17 @@ __device__ __forceinline__ void load_in(cx (&u)[16], const cx* buf, int i)
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
 // X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
 // barrier: a buffer is rewritten only after the barrier that follows its last read.
-__device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const cx* twA,
-                                        const cx* twB, int i)
+__device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const cx* tw, int i)
 {
-    pass_out<1>(u, buf0, twA, twB, i);
+    pass_out<1>(u, buf0, tw, i);
     __syncthreads();
     load_in(u, buf0, i);
-    pass_out<16>(u, buf1, twA, twB, i);
+    pass_out<16>(u, buf1, tw, i);
     __syncthreads();
     load_in(u, buf1, i);
     // span 256: k = i, outputs at i + 256 m stay in this thread
     cx w[16];
-    twiddle_powers(w, twA, twB, i);
+    twiddle_powers(w, tw + kTwL, 256, i);
 #pragma unroll
     for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
     dft16(u);
@@ -362,26 +357,23 @@ __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const c
 // ASYNC (rows 16-byte aligned, Nu % 4 == 0): the next row pair is fetched into a shared
 // staging buffer with cp.async while the current pair is transformed, hiding HBM latency.
 constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
-constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float2) * (256 + 16) +
+constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float2) * f4k::kTwEntries +
                             sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage;
 
 template <bool ASYNC>
 __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p,
-                                                            const float2* __restrict__ twA_g,
-                                                            const float2* __restrict__ twB_g,
+                                                            const float2* __restrict__ tw_g,
                                                             const float* __restrict__ Hs_g)
 {
     using namespace f4k;
     extern __shared__ __align__(16) unsigned char fsm[];
     cx* const buf = reinterpret_cast<cx*>(fsm);  // 2 x (L + L/16) (padded)
     cx* const bufB = buf + (L + L / 16);
-    cx* const twA = bufB + (L + L / 16);          // 256
-    cx* const twB = twA + 256;                    // 16
-    float* const Hs = reinterpret_cast<float*>(twB + 16);   // L/2 + 1 (2052 slots)
+    cx* const tw = bufB + (L + L / 16);           // kTwEntries
+    float* const Hs = reinterpret_cast<float*>(tw + kTwEntries);  // L/2 + 1 (2052 slots)
     float* const stage = Hs + 2052;                         // 2 rows
     const int i = threadIdx.x;
-    twA[i] = reinterpret_cast<const cx*>(twA_g)[i];
-    if (i < 16) twB[i] = reinterpret_cast<const cx*>(twB_g)[i];
+    for (int e = i; e < kTwEntries; e += T) tw[e] = reinterpret_cast<const cx*>(tw_g)[e];
     for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
     const long n_pairs = (p.n_rows_total + 1) / 2;
     auto prefetch = [&](long pr) {
@@ -430,7 +422,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
         }
         __syncthreads();  // staging read and buffers free: fetch the next pair meanwhile
         prefetch(pr + gridDim.x);
-        fft4096(u, buf, bufB, twA, twB, i);
+        fft4096(u, buf, bufB, tw, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -438,7 +430,7 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             const float h = Hs[f <= L / 2 ? f : L - f];
             u[m] = cmul2(u[m], mk(h, -h));
         }
-        fft4096(u, buf, bufB, twA, twB, i);  // buf's last reader was before bufB's barrier
+        fft4096(u, buf, bufB, tw, i);  // buf's last reader was before bufB's barrier
         // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1 (to every destination
         // band that holds the row when scattering).
         const int nd = p.n_dest > 0 ? p.n_dest : 1;
@@ -481,20 +473,21 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
             e = cudaMemcpy(D.tw, g->tw.data(), sizeof(float2) * L, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(filter tables)");
             if (L == 4096) {
-                std::vector<float> a(512), b(32);
-                for (int q = 0; q < 256; ++q) {
-                    a[2 * q] = g->tw[2 * (16 * q)];
-                    a[2 * q + 1] = g->tw[2 * (16 * q) + 1];
-                }
-                for (int q = 0; q < 16; ++q) {
-                    b[2 * q] = g->tw[2 * q];
-                    b[2 * q + 1] = g->tw[2 * q + 1];
-                }
-                if ((e = cudaMalloc(&D.twA, sizeof(float2) * 256)) != cudaSuccess ||
-                    (e = cudaMalloc(&D.twB, sizeof(float2) * 16)) != cudaSuccess)
+                // f4k twiddle tables: TL[q][i] = w^(2^q i), T16[q][k] = w^(16 2^q k)
+                std::vector<float> a(2 * f4k::kTwEntries);
+                auto put = [&](int slot, long ex) {
+                    const long t = ex % 4096;
+                    a[2 * slot] = g->tw[2 * t];
+                    a[2 * slot + 1] = g->tw[2 * t + 1];
+                };
+                for (int q = 0; q < 4; ++q)
+                    for (int ii = 0; ii < 256; ++ii) put(f4k::kTwL + q * 256 + ii, (long)(1 << q) * ii);
+                for (int q = 0; q < 4; ++q)
+                    for (int k = 0; k < 16; ++k) put(f4k::kTw16 + q * 16 + k, 16L * (1 << q) * k);
+                if ((e = cudaMalloc(&D.twA, sizeof(float2) * f4k::kTwEntries)) != cudaSuccess)
                     return cuda_fail(e, "cudaMalloc(twiddles)");
-                cudaMemcpy(D.twA, a.data(), sizeof(float2) * 256, cudaMemcpyHostToDevice);
-                e = cudaMemcpy(D.twB, b.data(), sizeof(float2) * 16, cudaMemcpyHostToDevice);
+                e = cudaMemcpy(D.twA, a.data(), sizeof(float2) * f4k::kTwEntries,
+                               cudaMemcpyHostToDevice);
                 if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(filter tables)");
             }
         }
@@ -534,8 +527,7 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
         auto k = async ? filter_f4k_kernel<true> : filter_f4k_kernel<false>;
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4kSmem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
-        k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].twA, g->dev[dev].twB,
-                                                 g->dev[dev].Hs);
+        k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].twA, g->dev[dev].Hs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "filter_f4k_kernel launch");
         count_launch();
