@@ -155,6 +155,17 @@ ifdk_status ifdk_backproject_alg2(const ifdk_geometry* g, const float* filtered_
                                   long n_views, float* vol_dev, int k0, int nk, int accumulate,
                                   int texture, void* stream);
 
+/* MEASURED BASELINE (not the production path): the paper's proposed Alg. alg:bp-v1
+ * as printed, in fp32 like the paper: per column and view the two
+ * inner products x, z, then per k < N_z/2 the one inner product y and the mirrored
+ * sample for slice N_z-1-k (Theorem 1, v~ = N_v-1-v).  Whole volume only ([Nz][Ny][Nx]);
+ * filtered_dev as for ifdk_backproject_alg2 (all N_v rows); texture = 1 samples through
+ * the texture unit.  Kept to re-measure the paper's claimed speed-up of Alg. alg:bp-v1
+ * over Alg. alg:bp on B200.  Errors as ifdk_backproject_alg2. */
+ifdk_status ifdk_backproject_alg4(const ifdk_geometry* g, const float* filtered_dev, long s0,
+                                  long n_views, float* vol_dev, int accumulate, int texture,
+                                  void* stream);
+
 /* ---- iterative reconstruction (SART / SIRT) ---- */
 
 /* The matched forward projector: the exact transpose of ifdk_backproject

@@ -225,6 +225,24 @@ extern "C" ifdk_status ifdk_backproject_alg2(const ifdk_geometry* g, const float
                                    texture, (cudaStream_t)stream);
 }
 
+extern "C" ifdk_status ifdk_backproject_alg4(const ifdk_geometry* g, const float* filtered_dev,
+                                             long s0, long n_views, float* vol_dev, int accumulate,
+                                             int texture, void* stream)
+{
+    t_launches = 0;
+    if (!g || !vol_dev || (!filtered_dev && n_views > 0))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if ((accumulate != 0 && accumulate != 1) || (texture != 0 && texture != 1))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "accumulate and texture must be 0 or 1");
+    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    if (n_views == 0) return launch_backproject(g, filtered_dev, s0, 0, 0, g->Nv, vol_dev, 0,
+                                                g->Nz, accumulate, (cudaStream_t)stream);
+    return launch_backproject_alg4(g, filtered_dev, s0, n_views, vol_dev, accumulate, texture,
+                                   (cudaStream_t)stream);
+}
+
 extern "C" ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw_dev,
                                         long n_views, float* vol_dev, void* stream)
 {

@@ -79,5 +79,7 @@ ifdk_status launch_fill(float* x, float value, long n, cudaStream_t st);
 ifdk_status launch_backproject_alg2(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                     float* vol, int k0, int nk, int accumulate, int hw,
                                     cudaStream_t st);
+ifdk_status launch_backproject_alg4(const ifdk_geometry* g, const float* Q, long s0, long n_views,
+                                    float* vol, int accumulate, int hw, cudaStream_t st);
 
 }  // namespace ifdk

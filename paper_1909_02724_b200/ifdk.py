@@ -37,6 +37,7 @@ EXPORTS = (
     "ifdk_filter_scatter",
     "ifdk_backproject",
     "ifdk_backproject_alg2",
+    "ifdk_backproject_alg4",
     "ifdk_reconstruct",
     "ifdk_reconstruct_host",
     "ifdk_forward_project",
@@ -81,6 +82,8 @@ _lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp
 _lib.ifdk_backproject.restype = _i
 _lib.ifdk_backproject_alg2.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _i, _i, _vp]
 _lib.ifdk_backproject_alg2.restype = _i
+_lib.ifdk_backproject_alg4.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _vp]
+_lib.ifdk_backproject_alg4.restype = _i
 _lib.ifdk_reconstruct.argtypes = [_vp, _vp, _l, _vp, _vp]
 _lib.ifdk_reconstruct.restype = _i
 _lib.ifdk_reconstruct_host.argtypes = [_vp, _vp, _l, _vp, _vp]
@@ -216,6 +219,20 @@ def ifdk_backproject_alg2(g: Geometry, filtered, s0: int, vol, k0: int = 0,
     _check(_lib.ifdk_backproject_alg2(g.handle, _dev_f32(filtered, "filtered"), int(s0),
                                       filtered.shape[0], _dev_f32(vol, "vol"), int(k0),
                                       vol.shape[0], 1 if accumulate else 0, 1 if texture else 0,
+                                      _stream_ptr(stream)))
+
+
+def ifdk_backproject_alg4(g: Geometry, filtered, s0: int, vol, accumulate: bool = False,
+                          texture: bool = False, stream=None) -> None:
+    """MEASURED BASELINE: the paper's Alg. alg:bp-v1 (fp32, mirror k-pairs) over the whole
+    volume; filtered [n][Nv][Nu], vol [Nz][Ny][Nx]."""
+    if filtered.dim() != 3 or filtered.shape[1] != g.Nv or filtered.shape[2] != g.Nu:
+        raise ValueError("filtered must be [n_views][Nv][Nu]")
+    if tuple(vol.shape) != (g.Nz, g.Ny, g.Nx):
+        raise ValueError("vol must be [Nz][Ny][Nx]")
+    _check(_lib.ifdk_backproject_alg4(g.handle, _dev_f32(filtered, "filtered"), int(s0),
+                                      filtered.shape[0], _dev_f32(vol, "vol"),
+                                      1 if accumulate else 0, 1 if texture else 0,
                                       _stream_ptr(stream)))
 
 

@@ -61,3 +61,31 @@ def test_alg2_baseline_vs_oracle_config1(torch_cuda, texture):
     ifdk_backproject_alg2(g, Qd[40:].contiguous(), 40, half, k0=16, accumulate=True,
                           texture=texture)
     assert torch.allclose(half, base[16:16 + spec.Nz // 2], rtol=1e-5, atol=1e-6 * float(base.abs().max()))
+
+
+@pytest.mark.parametrize("texture", [False, True])
+@pytest.mark.parametrize("dims", [(64, 64, 64, 64, 64, 64), (40, 48, 48, 36, 30, 33)])
+def test_alg4_baseline_vs_oracle(torch_cuda, texture, dims):
+    """The paper's Alg. alg:bp-v1 (mirror k-pairs, one inner product per k) computes Alg.
+    alg:bp: against the fp64 oracle within its fp32 / texture error, on an even N_z (config 1)
+    and an odd N_z (the middle slice is its own mirror)."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject_alg4
+
+    Np, Nu, Nv, Nx, Ny, Nz = dims
+    spec = synth.ConfigSpec("alg4", Np, Nu, Nv, Nx, Ny, Nz)
+    g = Geometry.from_spec(spec)
+    E = synth.project(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta,
+                      synth.default_ellipsoids(spec), 0, spec.Np)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    Q = oracle.filter_fft(og, E).astype(np.float32)
+    ref = oracle.backproject_volume(og, Q.astype(np.float64))
+    vol = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+    ifdk_backproject_alg4(g, torch.from_numpy(Q).cuda(), 0, vol, texture=texture)
+    rb, mb = _errors(vol.cpu().numpy(), ref)
+    print(f"\nBASELINE {dims} alg4 {'texture' if texture else 'software'}: relRMSE {rb:.3e} "
+          f"max {mb:.3e}")
+    if texture:
+        assert 1e-5 < rb < 2e-2, rb
+    else:
+        assert rb < 1e-4, rb

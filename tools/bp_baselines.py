@@ -13,7 +13,7 @@ sys.path.insert(0, "tests")
 import oracle  # noqa: E402
 import synth  # noqa: E402
 from paper_1909_02724_b200 import (Geometry, ifdk_backproject, ifdk_backproject_alg2,  # noqa: E402
-                                   ifdk_filter)
+                                   ifdk_backproject_alg4, ifdk_filter)
 
 SEED = 20261017
 
@@ -41,7 +41,9 @@ def main():
     out = {}
     kinds = {"production": lambda g, Q, v: ifdk_backproject(g, Q, 0, v),
              "alg2_software": lambda g, Q, v: ifdk_backproject_alg2(g, Q, 0, v, texture=False),
-             "alg2_texture": lambda g, Q, v: ifdk_backproject_alg2(g, Q, 0, v, texture=True)}
+             "alg2_texture": lambda g, Q, v: ifdk_backproject_alg2(g, Q, 0, v, texture=True),
+             "alg4_software": lambda g, Q, v: ifdk_backproject_alg4(g, Q, 0, v, texture=False),
+             "alg4_texture": lambda g, Q, v: ifdk_backproject_alg4(g, Q, 0, v, texture=True)}
     # timing: 256 views of configs 3 and 4
     for cfg in (3, 4):
         spec = synth.config(cfg)
