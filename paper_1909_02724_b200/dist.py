@@ -36,6 +36,21 @@ from typing import Callable, Optional
 KC = 64          # slab starts are multiples of the BP kernel k-chunk (32 or 64, backproject.cu)
 VIEW_BATCH = 128  # two-level summation batch of the BP kernel (BPParams.vb)
 D2H_SUBSLAB = 256  # slices per device-to-host piece of the end-to-end driver (multiple of KC)
+D2H_TAIL = 64      # ... and per piece of the slab's last 256 slices (the D2H nothing overlaps)
+
+
+def _d2h_pieces(k0: int, nk: int) -> list:
+    """(first slice, slices) pieces of slab k0..k0+nk-1 for the streamed D2H of the last
+    round: D2H_SUBSLAB-slice pieces, the last D2H_SUBSLAB slices in D2H_TAIL-slice ones
+    (all boundaries stay multiples of 64 relative to k0, so the result is unchanged)."""
+    out, a, end = [], k0, k0 + nk
+    while a + 2 * D2H_SUBSLAB <= end:
+        out.append((a, D2H_SUBSLAB))
+        a += D2H_SUBSLAB
+    while a < end:
+        out.append((a, min(D2H_TAIL, end - a)))
+        a += D2H_TAIL
+    return out
 
 
 def _split(n: int, parts: int, quantum: int) -> list[int]:
@@ -390,8 +405,8 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
             last = t == rounds - 1
             # the last round goes in sub-slabs so that finished slices leave for the host early
             subs = [(k0, nk)]
-            if last and vol_host is not None and nk > D2H_SUBSLAB:
-                subs = [(a, min(D2H_SUBSLAB, k0 + nk - a)) for a in range(k0, k0 + nk, D2H_SUBSLAB)]
+            if last and vol_host is not None and nk > D2H_TAIL:
+                subs = _d2h_pieces(k0, nk)
             launched = False
             for (a, m) in subs:
                 acc_first = first_bp
