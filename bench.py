@@ -467,6 +467,29 @@ def run_ours(args, spec, rank, world, local_rank):
         e2e = {"value": gups(spec, e2e_s), "unit": "GUPS", "seconds": e2e_s,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": n_e2e, "api": api}
+        # The host legs alone (pinned memory, 4 GiB each way through the same buffers), to
+        # state how much of them the pipeline hides: serial = device step + H2D + D2H.
+        try:
+            n = min(vol.numel(), raw_h.numel(), 1 << 30)
+            dv, rh, vh = vol.view(-1)[:n], raw_h.view(-1)[:n], vol_h.view(-1)[:n]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            dv.copy_(rh, non_blocking=True)
+            a.record()
+            dv.copy_(rh, non_blocking=True)
+            b.record()
+            b.synchronize()
+            h2d_gbs = 4 * n / (a.elapsed_time(b) / 1e3) / 1e9
+            a.record()
+            vh.copy_(dv, non_blocking=True)
+            b.record()
+            b.synchronize()
+            d2h_gbs = 4 * n / (a.elapsed_time(b) / 1e3) / 1e9
+            legs_s = h2d / world / 1e9 / h2d_gbs + d2h / world / 1e9 / d2h_gbs
+            e2e["host_legs"] = {"h2d_gbs": h2d_gbs, "d2h_gbs": d2h_gbs,
+                                "serial_seconds": ms / 1e3 + legs_s,
+                                "hidden_fraction": max(0.0, 1 - (e2e_s - ms / 1e3) / legs_s)}
+        except Exception as exc:  # noqa: BLE001 -- a report, never a reason to fail the bench
+            e2e["host_legs"] = {"error": repr(exc)[:200]}
         del raw_h, vol_h
 
     # The projection-split and R x C grid variants, measured against the slab split in the
