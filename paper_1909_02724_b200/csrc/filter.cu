@@ -360,32 +360,41 @@ constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
 constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float2) * f4k::kTwEntries +
                             sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage;
 
-template <bool ASYNC>
+// R row pairs per transform (multi-row packing): with N_u <= 2048 / R every row's linear
+// convolution needs only a 2 N_u - 1 window of the length-4096 circular one, so R rows share
+// the real part (and R the imaginary part) in slots of S = 4096 / R samples: the ramp's
+// support (|n - m| <= N_u - 1) never reaches from one slot into another (S - N_u >= N_u - 1),
+// and each slot's first N_u outputs are exactly that row's linear convolution.  Configs 2 / 3
+// (N_u = 512 / 1024) run 4 / 2 row pairs per transform.
+template <bool ASYNC, int R>
 __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p,
                                                             const float2* __restrict__ tw_g,
                                                             const float* __restrict__ Hs_g)
 {
     using namespace f4k;
+    constexpr int SJ = 16 / R;          // values j of a thread per slot (slot = S / 256 j's)
+    constexpr int ROWS = 2 * R;         // rows per transform
+    constexpr int SLOT_F = 4096 / ROWS; // staged floats per row (>= N_u)
     extern __shared__ __align__(16) unsigned char fsm[];
     cx* const buf = reinterpret_cast<cx*>(fsm);  // 2 x (L + L/16) (padded)
     cx* const bufB = buf + (L + L / 16);
     cx* const tw = bufB + (L + L / 16);           // kTwEntries
     float* const Hs = reinterpret_cast<float*>(tw + kTwEntries);  // L/2 + 1 (2052 slots)
-    float* const stage = Hs + 2052;                         // 2 rows
+    float* const stage = Hs + 2052;                                // ROWS rows of SLOT_F
     const int i = threadIdx.x;
     for (int e = i; e < kTwEntries; e += T) tw[e] = reinterpret_cast<const cx*>(tw_g)[e];
     for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
-    const long n_pairs = (p.n_rows_total + 1) / 2;
-    auto prefetch = [&](long pr) {
-        if (!ASYNC || pr >= n_pairs) return;
-        const long rA = 2 * pr;
-        const int nrow = (2 * pr + 1 < p.n_rows_total) ? 2 : 1;
+    const long n_groups = (p.n_rows_total + ROWS - 1) / ROWS;
+    auto prefetch = [&](long gi) {
+        if (!ASYNC || gi >= n_groups) return;
+        const long r0 = ROWS * gi;
+        const int nrow = (int)min((long)ROWS, p.n_rows_total - r0);
         const int q4 = p.Nu / 4;
         for (int c = i; c < nrow * q4; c += T) {
-            const int r = c >= q4, cc = c - r * q4;
-            const float* src = p.raw + (rA + r) * p.Nu + 4 * cc;
+            const int r = c / q4, cc = c - r * q4;
+            const float* src = p.raw + (r0 + r) * p.Nu + 4 * cc;
             const uint32_t dst =
-                static_cast<uint32_t>(__cvta_generic_to_shared(stage + r * kF4kStage + 4 * cc));
+                static_cast<uint32_t>(__cvta_generic_to_shared(stage + r * SLOT_F + 4 * cc));
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src)
                          : "memory");
         }
@@ -393,35 +402,46 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
     };
     prefetch(blockIdx.x);
     __syncthreads();
-    for (long pr = blockIdx.x; pr < n_pairs; pr += gridDim.x) {
-        const long rA = 2 * pr, rB = 2 * pr + 1;
-        const bool hasB = rB < p.n_rows_total;
-        const float vhA = ((float)(p.v0 + (int)(rA % p.n_rows)) - p.cv) * p.Dv;
-        const float vhB = ((float)(p.v0 + (int)(rB % p.n_rows)) - p.cv) * p.Dv;
-        const float dA = p.D2 + vhA * vhA, dB = p.D2 + vhB * vhB;
-        const float* eA = ASYNC ? stage : p.raw + rA * p.Nu;
-        const float* eB = ASYNC ? stage + kF4kStage : p.raw + rB * p.Nu;
+    for (long gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
+        const long r0 = ROWS * gi;
+        // per slot s: rows A = r0 + 2s (real part), B = r0 + 2s + 1 (imaginary part)
+        float dA[R], dB[R];
+#pragma unroll
+        for (int sl = 0; sl < R; ++sl) {
+            const long rA = r0 + 2 * sl, rB = rA + 1;
+            const float vhA = ((float)(p.v0 + (int)(rA % p.n_rows)) - p.cv) * p.Dv;
+            const float vhB = ((float)(p.v0 + (int)(rB % p.n_rows)) - p.cv) * p.Dv;
+            dA[sl] = p.D2 + vhA * vhA;
+            dB[sl] = p.D2 + vhB * vhB;
+        }
         if (ASYNC) {
             asm volatile("cp.async.wait_all;" ::: "memory");
             __syncthreads();
         }
         cx u[16];
-        // Alg. alg:filter line 2: E~ = E . F_cos (reading c-A5), rows A | B packed, zero padded.
+        // Alg. alg:filter line 2: E~ = E . F_cos (reading c-A5), rows packed per slot, padded.
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            const int n = i + j * T;
+            const int sl = j / SJ;
+            const int n = i + (j % SJ) * T;
+            const long rA = r0 + 2 * sl, rB = rA + 1;
             float2 x = make_float2(0.f, 0.f);  // (row A, row B)
-            if (j < 8 && n < p.Nu) {
+            if ((R > 1 || j < 8) && n < p.Nu && rA < p.n_rows_total) {
                 const float uh = ((float)n - p.cu) * p.Du;
                 // F_cos = D / sqrt(D^2 + uh^2 + vh^2); rsqrtf's <= 2 ulp error is far below the
                 // filter tolerance and saves the IEEE sqrt + divide sequences.
-                x.x = (ASYNC ? eA[n] : __ldg(eA + n)) * (p.D * rsqrtf(fmaf(uh, uh, dA)));
-                if (hasB) x.y = (ASYNC ? eB[n] : __ldg(eB + n)) * (p.D * rsqrtf(fmaf(uh, uh, dB)));
+                const float ea = ASYNC ? stage[(2 * sl) * SLOT_F + n] : __ldg(p.raw + rA * p.Nu + n);
+                x.x = ea * (p.D * rsqrtf(fmaf(uh, uh, dA[sl])));
+                if (rB < p.n_rows_total) {
+                    const float eb =
+                        ASYNC ? stage[(2 * sl + 1) * SLOT_F + n] : __ldg(p.raw + rB * p.Nu + n);
+                    x.y = eb * (p.D * rsqrtf(fmaf(uh, uh, dB[sl])));
+                }
             }
             u[j] = mk(x.x, x.y);
         }
-        __syncthreads();  // staging read and buffers free: fetch the next pair meanwhile
-        prefetch(pr + gridDim.x);
+        __syncthreads();  // staging read and buffers free: fetch the next group meanwhile
+        prefetch(gi + gridDim.x);
         fft4096(u, buf, bufB, tw, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
 #pragma unroll
@@ -431,18 +451,26 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             u[m] = cmul2(u[m], mk(h, -h));
         }
         fft4096(u, buf, bufB, tw, i);  // buf's last reader was before bufB's barrier
-        // Q = conj(Z): real -> row A, -imag -> row B, samples 0..Nu-1 (to every destination
-        // band that holds the row when scattering).
+        // Q = conj(Z): real -> row A, -imag -> row B of each slot, samples 0..Nu-1 (to every
+        // destination band that holds the row when scattering).
         const int nd = p.n_dest > 0 ? p.n_dest : 1;
         for (int d = 0; d < nd; ++d) {
-            float* qA = p.n_dest > 0 ? dest_row(p, rA, d) : p.out + rA * p.Nu;
-            float* qB = !hasB ? nullptr : p.n_dest > 0 ? dest_row(p, rB, d) : p.out + rB * p.Nu;
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
-                const int n = i + m * T;
-                if (n < p.Nu) {
-                    if (qA) qA[n] = re_(u[m]);
-                    if (qB) qB[n] = -im_(u[m]);
+            for (int sl = 0; sl < R; ++sl) {
+                const long rA = r0 + 2 * sl, rB = rA + 1;
+                if (rA >= p.n_rows_total) break;
+                float* qA = p.n_dest > 0 ? dest_row(p, rA, d) : p.out + rA * p.Nu;
+                float* qB = rB >= p.n_rows_total ? nullptr
+                            : p.n_dest > 0      ? dest_row(p, rB, d)
+                                                : p.out + rB * p.Nu;
+#pragma unroll
+                for (int jj = 0; jj < (R > 1 ? SJ : 8); ++jj) {
+                    const int m = sl * SJ + jj;
+                    const int n = i + jj * T;
+                    if (n < p.Nu) {
+                        if (qA) qA[n] = re_(u[m]);
+                        if (qB) qB[n] = -im_(u[m]);
+                    }
                 }
             }
         }
@@ -518,13 +546,23 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
     }
     const long pairs = (total + 1) / 2;
     if (L == 4096) {
+        // row pairs per transform: the largest R <= 8 whose slot 4096 / R holds a full-length
+        // linear convolution of an N_u-sample row (4096 / R >= 2 N_u - 1)
+        int R = 1;
+        while (R < 8 && 4096 / (2 * R) >= 2 * g->Nu - 1) R *= 2;
+        const long groups = (total + 2 * R - 1) / (2 * R);
         long grid = (long)sms * 2;
-        if (grid > pairs) grid = pairs;
-        // In-place filtering is safe with the prefetch: a pair's rows are fetched before any
-        // CTA writes them (each pair belongs to one CTA) and never read again.  (A scatter
+        if (grid > groups) grid = groups;
+        // In-place filtering is safe with the prefetch: a group's rows are fetched before any
+        // CTA writes them (each group belongs to one CTA) and never read again.  (A scatter
         // destination must not alias the raw views.)
         const bool async = (g->Nu % 4) == 0 && (reinterpret_cast<uintptr_t>(raw) % 16) == 0;
-        auto k = async ? filter_f4k_kernel<true> : filter_f4k_kernel<false>;
+        auto pick = [&](auto ka, auto ks) { return async ? ka : ks; };
+        void (*k)(const FilterParams, const float2*, const float*) =
+            R == 8   ? pick(filter_f4k_kernel<true, 8>, filter_f4k_kernel<false, 8>)
+            : R == 4 ? pick(filter_f4k_kernel<true, 4>, filter_f4k_kernel<false, 4>)
+            : R == 2 ? pick(filter_f4k_kernel<true, 2>, filter_f4k_kernel<false, 2>)
+                     : pick(filter_f4k_kernel<true, 1>, filter_f4k_kernel<false, 1>);
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4kSmem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
         k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].twA, g->dev[dev].Hs);
