@@ -59,6 +59,7 @@ __device__ __forceinline__ void red_add_if(uint32_t addr, int v, uint32_t pred)
 struct __align__(16) Box {
     int u_org, v_org, w, h;
 };
+constexpr int kBoxRing = 16;
 
 template <bool SMALL_DV>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -81,8 +82,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, kKC);
     const bool full = kv0 == 0 && kv1 == kKC;
     const int cap = p.box_w * p.box_h;
-    Box* const box = reinterpret_cast<Box*>(fsm);  // four slots (t & 3)
-    float* const wmax = fsm + 4 * sizeof(Box) / sizeof(float);  // 8 per-warp maxima
+    Box* const box = reinterpret_cast<Box*>(fsm);  // ring of kBoxRing slots (t & 15)
+    float* const wmax = fsm + kBoxRing * sizeof(Box) / sizeof(float);  // 8 per-warp maxima
     int* const patch0 = reinterpret_cast<int*>(wmax + 8);       // two buffers of cap ints
 
     // this column's voxels (0 outside the slab / volume): x(i, j, kb + kk)
@@ -110,8 +111,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     const float scale = ldexpf(1.f, 30 - ex), inv_scale = ldexpf(1.f, ex - 30);
     // patch box of view t: lanes 0-3 of warp 0 take the tile's corner columns at both chunk
     // ends (u, v are linear-fractional in the column position: extremes sit at corners)
+    // Boxes are computed 8 views at a time, one view per warp (no warp waits at the per-view
+    // barrier for another's fp64 corner math).
     auto make_box = [&](int t) {
-        if (warp != 0 || t >= p.n_views) return;
+        if (t >= p.n_views) return;
         const int c = lane & 3;
         const double ci = (c & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
         const double cj = (c & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
@@ -133,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             b.w = (int)floor(umax) - b.u_org + 3;
             b.h = (int)floor(vmax) - b.v_org + 3;
             if (b.w > p.box_w || b.h > p.box_h) __trap();  // the host bound is conservative
-            box[t & 3] = b;
+            box[t & (kBoxRing - 1)] = b;
         }
     };
     // add the patch of view t to the projection (non-zero, on-detector, in-band taps) and
@@ -141,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int r0 = tid / p.box_w, c0 = tid - r0 * p.box_w;
     const int dr = kThreads / p.box_w, dc = kThreads - dr * p.box_w;
     auto flush = [&](int t) {
-        const Box b = box[t & 3];
+        const Box b = box[t & (kBoxRing - 1)];
         int* const pa = patch0 + (t & 1) * cap;
         float* const pv = p.proj + (long)t * p.n_rows * p.Nu;
         // (r, c) of element e = tid + kThreads q stepped incrementally (no division per element)
@@ -163,12 +166,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
 
     for (int e = tid; e < 2 * cap; e += kThreads) patch0[e] = 0;
-    make_box(0);
+    make_box(warp);  // views 0 .. 7
     __syncthreads();
     // One barrier per view: splat view t into buffer t & 1 while view t-1's buffer is flushed
     // and the box of view t+1 is computed.
     for (int t = 0; t < p.n_views; ++t) {
-        const Box b = box[t & 3];
+        const Box b = box[t & (kBoxRing - 1)];
         int* const pa = patch0 + (t & 1) * cap;
         const ThreadInv ti = split(column_invariants(pt.P[t], di, dj, (double)kb));
         int* const base = pa + (ti.nv - b.v_org) * p.box_w + (ti.nu - b.u_org);
@@ -264,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             add_row(cur + 1, B);
         }
         if (t > 0) flush(t - 1);
-        make_box(t + 1);
+        // views t+2 .. t+9 (slots of views t-1, t in use; t+1 already computed)
+        if (((t + 2) & 7) == 0) make_box(t + 2 + warp);
         __syncthreads();
     }
     if (p.n_views > 0) flush(p.n_views - 1);
@@ -296,7 +300,8 @@ ifdk_status launch_forward_project(const ifdk_geometry* g, const float* vol, int
     patch_bound(g, kTI, kTJ, kKC, &wb, &hb);
     p.box_w = (int)std::ceil(wb) + 6;
     p.box_h = (int)std::ceil(hb) + 6;
-    const size_t smem = sizeof(int) * 2 * (size_t)p.box_w * p.box_h + 4 * sizeof(Box) + 8 * sizeof(float);
+    const size_t smem =
+        sizeof(int) * 2 * (size_t)p.box_w * p.box_h + kBoxRing * sizeof(Box) + 8 * sizeof(float);
     const double dv_min = g->D * g->Dz / (g->Dv * g->zmax);
     p.qfactor = (float)(256.0 * (1.0 / dv_min + 1.0) / (g->zmin * g->zmin));
     if (smem > 200 * 1024) return fail(IFDK_ERR_INVALID_ARGUMENT, "forward projector patch too large");
