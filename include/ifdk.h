@@ -155,6 +155,19 @@ ifdk_status ifdk_backproject_alg2(const ifdk_geometry* g, const float* filtered_
                                   long n_views, float* vol_dev, int k0, int nk, int accumulate,
                                   int texture, void* stream);
 
+/* The k-slab split without any exchange ("zero-exchange"): the volume slab
+ * k0..k0+nk-1 reconstructed from host views by copying only the detector row band the slab
+ * needs (ifdk_band_rows over all views; filtering is row-separable, Alg. alg:filter line 3,
+ * P:396), filtering it and back-projecting it -- what one GPU of an N-GPU split does with no
+ * inter-GPU traffic at all.  raw_host: [n_views][Nv][Nu] fp32 host (pinned for overlap);
+ * vol_host: [nk][Ny][Nx] fp32 host.  Pipelined like ifdk_reconstruct_host; synchronous.
+ * Values equal ifdk_reconstruct's slab within fp32 rounding (rows pair up differently in the
+ * filter's complex transforms).  Errors: INVALID_ARGUMENT (NULL), SHAPE (slab outside
+ * [0, Nz), n_views < 0), OUT_OF_MEMORY. */
+ifdk_status ifdk_reconstruct_slab_host(const ifdk_geometry* g, const float* raw_host,
+                                       long n_views, int k0, int nk, float* vol_host,
+                                       void* stream);
+
 /* MEASURED BASELINE (not the production path): the paper's proposed Alg. alg:bp-v1
  * as printed, in fp32 like the paper: per column and view the two
  * inner products x, z, then per k < N_z/2 the one inner product y and the mirrored

@@ -18,6 +18,7 @@ from .ifdk import (  # noqa: F401
     ifdk_forward_project,
     ifdk_reconstruct,
     ifdk_reconstruct_host,
+    ifdk_reconstruct_slab_host,
     ifdk_sart_ratio,
     ifdk_sart_update,
     last_launch_count,

@@ -273,17 +273,18 @@ extern "C" ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw
     return s;
 }
 
-extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float* raw_host,
-                                             long n_views, float* vol_host, void* stream)
+// End-to-end reconstruction of the slab k0..k0+nk-1 from host views, copying only detector
+// rows v0..v0+n_rows-1 of each view (the full detector for ifdk_reconstruct_host; the slab's
+// row band for ifdk_reconstruct_slab_host).
+static ifdk_status reconstruct_host_impl(const ifdk_geometry* g, const float* raw_host,
+                                         long n_views, int k0s, int nks, int v0, int n_rows,
+                                         float* vol_host, cudaStream_t st)
 {
-    t_launches = 0;
-    if (!g || !raw_host || !vol_host) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
-    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
-    ifdk_status s = need_device();
-    if (s != IFDK_OK) return s;
-    cudaStream_t st = (cudaStream_t)stream;
-    const size_t view_elems = (size_t)g->Nv * g->Nu;
-    const size_t vol_elems = (size_t)g->Nz * g->Ny * g->Nx;
+    ifdk_status s = IFDK_OK;
+    const size_t view_elems = (size_t)n_rows * g->Nu;          // staged elements per view
+    const size_t host_view_elems = (size_t)g->Nv * g->Nu;      // elements per host view
+    const size_t plane = (size_t)g->Ny * g->Nx;
+    const size_t vol_elems = (size_t)nks * plane;
     const long batch = n_views < kViewBatch ? (n_views > 0 ? n_views : 1) : kViewBatch;
     // Two staging buffers: batch b+1 is copied on `cp` while batch b is filtered (in place)
     // and back-projected on `st`.
@@ -310,7 +311,7 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
         cudaEventRecord(ready, st);  // allocations visible to the copy stream
         cudaStreamWaitEvent(cp, ready, 0);
         cudaEventDestroy(ready);
-        if (n_views == 0) s = launch_backproject(g, buf[0], 0, 0, 0, g->Nv, vol, 0, g->Nz, 0, st);
+        if (n_views == 0) s = launch_backproject(g, buf[0], 0, 0, v0, n_rows, vol, k0s, nks, 0, st);
         // Batches of `batch` views, the first full batch split in two halves (views 0..127,
         // 128..255, one per staging buffer) so that the one H2D nothing overlaps is half a
         // batch; the last batch stays full, so its back-projection still covers the volume's
@@ -330,8 +331,11 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
             const long b0 = bat[b].first;
             const long nb = bat[b].second;
             if (b >= 2) cudaStreamWaitEvent(cp, consumed[q], 0);
-            cudaMemcpyAsync(buf[q], raw_host + b0 * view_elems, sizeof(float) * view_elems * nb,
-                            cudaMemcpyHostToDevice, cp);
+            // rows v0..v0+n_rows-1 of views b0..b0+nb-1: one 2-D copy (a contiguous run per view)
+            cudaMemcpy2DAsync(buf[q], sizeof(float) * view_elems,
+                              raw_host + b0 * host_view_elems + (size_t)v0 * g->Nu,
+                              sizeof(float) * host_view_elems, sizeof(float) * view_elems, nb,
+                              cudaMemcpyHostToDevice, cp);
             cudaEventRecord(copied[q], cp);
         };
         if (nbatches > 0) enqueue_copy(0);
@@ -341,10 +345,10 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
             const long b0 = bat[b].first;
             const long nb = bat[b].second;
             cudaStreamWaitEvent(st, copied[q], 0);
-            s = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb, 0, g->Nv, st);
+            s = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb, v0, n_rows, st);
             if (s != IFDK_OK) break;
             if (b + 1 < nbatches) {
-                s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vol, 0, g->Nz,
+                s = launch_backproject(g, buf[q], b0, nb, v0, n_rows, vol, k0s, nks,
                                        b0 > 0 ? 1 : 0, st);
             } else {
                 // Last batch: back-project slab by slab and stream each finished slab to the
@@ -353,22 +357,23 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
                 // 256-slice slabs, the last 256 slices in 64-slice ones: the final D2H, which
                 // nothing overlaps, is then a quarter of a slab.
                 std::vector<std::pair<int, int>> slabs;
-                if (g->Nz > 512) {
-                    int k0 = 0;
-                    for (; k0 + 512 <= g->Nz; k0 += 256) slabs.emplace_back(k0, 256);
-                    for (; k0 < g->Nz; k0 += 64) slabs.emplace_back(k0, std::min(64, g->Nz - k0));
+                const int kend = k0s + nks;
+                if (nks > 512) {
+                    int k0 = k0s;
+                    for (; k0 + 512 <= kend; k0 += 256) slabs.emplace_back(k0, 256);
+                    for (; k0 < kend; k0 += 64) slabs.emplace_back(k0, std::min(64, kend - k0));
                 } else {
-                    slabs.emplace_back(0, g->Nz);
+                    slabs.emplace_back(k0s, nks);
                 }
                 for (size_t si = 0; si < slabs.size() && s == IFDK_OK; ++si) {
                     const int k0 = slabs[si].first, nk = slabs[si].second;
-                    float* vs = vol + (size_t)k0 * g->Ny * g->Nx;
-                    s = launch_backproject(g, buf[q], b0, nb, 0, g->Nv, vs, k0, nk,
+                    float* vs = vol + (size_t)(k0 - k0s) * plane;
+                    s = launch_backproject(g, buf[q], b0, nb, v0, n_rows, vs, k0, nk,
                                            b0 > 0 ? 1 : 0, st);
                     cudaEventRecord(slab_done, st);
                     cudaStreamWaitEvent(cp, slab_done, 0);
-                    e = cudaMemcpyAsync(vol_host + (size_t)k0 * g->Ny * g->Nx, vs,
-                                        sizeof(float) * (size_t)nk * g->Ny * g->Nx,
+                    e = cudaMemcpyAsync(vol_host + (size_t)(k0 - k0s) * plane, vs,
+                                        sizeof(float) * (size_t)nk * plane,
                                         cudaMemcpyDeviceToHost, cp);
                     if (e != cudaSuccess) s = cuda_fail(e, "cudaMemcpyAsync(volume D2H)");
                 }
@@ -397,6 +402,47 @@ extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float
     cudaEventDestroy(slab_done);
     cudaStreamDestroy(cp);
     return s;
+}
+
+extern "C" ifdk_status ifdk_reconstruct_host(const ifdk_geometry* g, const float* raw_host,
+                                             long n_views, float* vol_host, void* stream)
+{
+    t_launches = 0;
+    if (!g || !raw_host || !vol_host) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    return reconstruct_host_impl(g, raw_host, n_views, 0, g->Nz, 0, g->Nv, vol_host,
+                                 (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_reconstruct_slab_host(const ifdk_geometry* g, const float* raw_host,
+                                                  long n_views, int k0, int nk, float* vol_host,
+                                                  void* stream)
+{
+    t_launches = 0;
+    if (!g || !raw_host || !vol_host) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (n_views < 0) return fail(IFDK_ERR_SHAPE, "n_views < 0");
+    if (k0 < 0 || nk < 1 || (long)k0 + nk > g->Nz)
+        return fail(IFDK_ERR_SHAPE, "slab k0..k0+nk-1 outside [0, Nz)");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    // the union of the rows the slab's taps can touch over all views
+    int lo = g->Nv, hi = -1;
+    for (long t = 0; t < n_views; ++t) {
+        int a, b;
+        band_rows(g, k0, nk, t, &a, &b);
+        if (a <= b) {
+            lo = std::min(lo, a);
+            hi = std::max(hi, b);
+        }
+    }
+    if (hi < lo) {  // no view reaches the slab: it is zero
+        lo = 0;
+        hi = 0;
+    }
+    return reconstruct_host_impl(g, raw_host, n_views, k0, nk, lo, hi - lo + 1, vol_host,
+                                 (cudaStream_t)stream);
 }
 
 extern "C" void ifdk_geometry_destroy(ifdk_geometry* g)

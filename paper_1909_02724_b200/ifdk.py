@@ -40,6 +40,7 @@ EXPORTS = (
     "ifdk_backproject_alg4",
     "ifdk_reconstruct",
     "ifdk_reconstruct_host",
+    "ifdk_reconstruct_slab_host",
     "ifdk_forward_project",
     "ifdk_sart_ratio",
     "ifdk_sart_update",
@@ -88,6 +89,8 @@ _lib.ifdk_reconstruct.argtypes = [_vp, _vp, _l, _vp, _vp]
 _lib.ifdk_reconstruct.restype = _i
 _lib.ifdk_reconstruct_host.argtypes = [_vp, _vp, _l, _vp, _vp]
 _lib.ifdk_reconstruct_host.restype = _i
+_lib.ifdk_reconstruct_slab_host.argtypes = [_vp, _vp, _l, _i, _i, _vp, _vp]
+_lib.ifdk_reconstruct_slab_host.restype = _i
 _lib.ifdk_forward_project.argtypes = [_vp, _vp, _i, _i, _l, _l, _vp, _i, _i, _i, _vp]
 _lib.ifdk_forward_project.restype = _i
 _lib.ifdk_sart_ratio.argtypes = [_vp, _vp, _vp, _vp, _l, _vp]
@@ -267,6 +270,19 @@ def ifdk_reconstruct_host(g: Geometry, raw_host, vol_host, stream=None) -> None:
     if tuple(vs) != (g.Nz, g.Ny, g.Nx):
         raise ValueError("vol_host must be [Nz][Ny][Nx]")
     _check(_lib.ifdk_reconstruct_host(g.handle, rp, rs[0], vp, _stream_ptr(stream)))
+
+
+def ifdk_reconstruct_slab_host(g: Geometry, raw_host, k0: int, vol_host, stream=None) -> None:
+    """Slab k0..k0+nk-1 (vol_host [nk][Ny][Nx], host) reconstructed from host views
+    raw_host [n][Nv][Nu] copying only the slab's detector row band (no exchange); synchronous."""
+    rp, rs = _host_f32(raw_host, "raw_host")
+    vp, vs = _host_f32(vol_host, "vol_host")
+    if len(rs) != 3 or rs[1] != g.Nv or rs[2] != g.Nu:
+        raise ValueError("raw_host must be [n_views][Nv][Nu]")
+    if len(vs) != 3 or vs[1] != g.Ny or vs[2] != g.Nx:
+        raise ValueError("vol_host must be [nk][Ny][Nx]")
+    _check(_lib.ifdk_reconstruct_slab_host(g.handle, rp, rs[0], int(k0), vs[0], vp,
+                                           _stream_ptr(stream)))
 
 
 def ifdk_forward_project(g: Geometry, vol, s0: int, proj, k0: int = 0, v0: int = 0,
