@@ -10,7 +10,8 @@ import torch.distributed as dist
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_1909_02724_b200 import Geometry, ifdk_reconstruct  # noqa: E402
-from paper_1909_02724_b200.dist import SlabPlan, kslab_reconstruct  # noqa: E402
+from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct,  # noqa: E402
+                                        kslab_reconstruct_host, projection_split_reconstruct)
 
 
 def main():
@@ -39,6 +40,26 @@ def main():
         bad += not ok
         print(f"KSLAB rank {rank}/{world} exchange={exchange} used={tm.get('exchange')} "
               f"bitwise={'OK' if ok else 'MISMATCH'} wall={tm.get('wall_ms', 0):.1f} ms", flush=True)
+    # end to end from pinned host memory (H2D one round ahead, D2H in sub-slabs)
+    raw_h = raw.cpu().pin_memory()
+    vol_h = torch.empty((nk, spec.Ny, spec.Nx), dtype=torch.float32, pin_memory=True)
+    vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
+    kslab_reconstruct_host(g, raw_h, vol, vol_h, plan, rank, force_exchange=True)
+    torch.cuda.synchronize()
+    ok = torch.equal(vol_h, ref[k0:k0 + nk].cpu())
+    bad += not ok
+    print(f"KSLAB-HOST rank {rank}/{world} bitwise={'OK' if ok else 'MISMATCH'}", flush=True)
+    # projection split: partial volume of the own views + NCCL reduce-scatter of k-slabs
+    if spec.Nz % world == 0:
+        ps = torch.empty((spec.Nz // world, spec.Ny, spec.Nx), device="cuda")
+        projection_split_reconstruct(g, raw, plan.local_views(rank), ps, world)
+        r0 = rank * spec.Nz // world
+        refp = ref[r0:r0 + spec.Nz // world]
+        err = float((ps - refp).abs().max() / ref.abs().max())
+        ok = err <= 1e-5
+        bad += not ok
+        print(f"PSPLIT rank {rank}/{world} max|d|/max|V|={err:.2e} {'OK' if ok else 'MISMATCH'}",
+              flush=True)
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
 
