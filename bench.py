@@ -594,6 +594,39 @@ def run_ours(args, spec, rank, world, local_rank):
                                 "kernel_launches": last_launch_count()}
             del oraw, ovol
         torch.cuda.empty_cache()
+        # Config 5 (4096 views of 2048^2 -> 4096^3, 256 GiB) only exists k-slab-partitioned over
+        # 8 GPUs; one GPU runs one rank's share: slab 0 (512 slices) from its row band, the
+        # first 256 views (filter + BP through the C ABI).
+        if args.config != 5:
+            from paper_1909_02724_b200 import ifdk_backproject, ifdk_filter
+
+            c5 = synth.config(5)
+            g5 = Geometry.from_spec(c5)
+            k0, nk, n5 = 0, c5.Nz // 8, 256
+            lo = min(g5.band_rows(k0, nk, s5)[0] for s5 in range(n5))
+            hi = max(g5.band_rows(k0, nk, s5)[1] for s5 in range(n5))
+            e5 = torch.empty((n5, hi - lo + 1, c5.Nu), device=dev)
+            synth.project_gpu(c5.Nu, c5.Nv, c5.Du, c5.Dv, c5.D, c5.d, c5.theta,
+                              synth.default_ellipsoids(c5), 0, n5, lo, hi - lo + 1,
+                              e5.data_ptr(), stream.cuda_stream)
+            v5 = torch.empty((nk, c5.Ny, c5.Nx), device=dev)
+            ts = []
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                q5 = e5.clone()
+                a.record()
+                ifdk_filter(g5, q5, q5, v0=lo)
+                ifdk_backproject(g5, q5, 0, v5, k0=k0, v0=lo)
+                b.record()
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+                del q5
+            t_ms = sorted(ts)[1]
+            others[f"{c5.name} (k-slab 0 of 8, 256 views)"] = {
+                "fdk_ms": t_ms, "gups": c5.Nx * c5.Ny * nk * n5 / (t_ms / 1e3) / 2 ** 30,
+                "band_rows": hi - lo + 1, "kernel_launches": 2}
+            del e5, v5
+            torch.cuda.empty_cache()
 
     # Iterative reconstruction: one SIRT iteration on config 3 (1024 views
     # of 1024^2 -> 1024^3) = forward projection + back-projection + element-wise steps, the
