@@ -713,7 +713,11 @@ def run_ours(args, spec, rank, world, local_rank):
         "roofline": {"bound": "smem", "achieved": achieved_gbs, "peak": peak_gbs,
                      "unit": "GB/s", "frac": achieved_gbs / peak_gbs,
                      "frac_vs_derived_peak": achieved_gbs / derived_gbs,
-                     "traffic": ncu_traffic(args.config),
+                     # per launch, scaled by updates from the captured 256-view full-depth
+                     # launch (k-slab rounds at N > 1 are smaller launches)
+                     "traffic": (ncu_traffic(args.config) * upd_per_launch
+                                 / (256.0 * spec.Nx * spec.Ny * spec.Nz)
+                                 if ncu_traffic(args.config) else None),
                      "kernel": "bp_raw_kernel (16 algorithmic B/update of bilinear taps)",
                      "peak_basis": peak_basis},
         "roofline_hbm": roofline_hbm,
