@@ -211,6 +211,18 @@ ifdk_status ifdk_sart_ratio(const float* b_dev, const float* ax_dev, const float
 ifdk_status ifdk_sart_update(float* x_dev, const float* c_dev, const float* C_dev, float lambda,
                              long n, int nonneg, void* stream);
 
+/* MLEM / OS-EM ratio step (Shepp & Vardi, cited at P:266; reading c-I4):
+ * out[e] = b[e] / ax[e] where ax[e] > 0, else 0.  ax = forward projection of the current
+ * estimate; out may alias ax.  Errors: INVALID_ARGUMENT (NULL), SHAPE (n < 0). */
+ifdk_status ifdk_mlem_ratio(const float* b_dev, const float* ax_dev, float* out_dev, long n,
+                            void* stream);
+
+/* MLEM / OS-EM multiplicative update (reading c-I4): x[e] = x[e] c[e] / C[e] where
+ * C[e] > 0 (C = back-projection of ones), else x[e] unchanged.  c = back-projection of
+ * the ratio.  Errors: INVALID_ARGUMENT (NULL), SHAPE (n < 0). */
+ifdk_status ifdk_mlem_update(float* x_dev, const float* c_dev, const float* C_dev, long n,
+                             void* stream);
+
 /* x[e] = value for n fp32 device elements (normaliser inputs of SART).
  * Errors: INVALID_ARGUMENT (NULL), SHAPE (n < 0). */
 ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream);

@@ -24,6 +24,8 @@ What it computes (all fp64; the only fp32 quantity is the raw input E):
   against ``backproject_volume`` and by closed forms.
 * ``sart``               -- SART / SIRT (Andersen & Kak, cited at P:266;
   readings c-I2, c-I3) built from the two operators.
+* ``mlem``               -- MLEM / OS-EM (Shepp & Vardi, cited at P:266; reading
+  c-I4), the multiplicative update from the same operators.
 
 Parity pins live in ``tests/test_oracle_pins.py``.  Functions whose result
 the paper does not fix (the F_cos formula, the ramp shape, the constant C,
@@ -41,6 +43,7 @@ from .oracle import (  # noqa: F401
     filter_fft,
     forward_project,
     interp2,
+    mlem,
     num_threads,
     projection_matrix,
     ramp_h1,

@@ -259,3 +259,23 @@ def sart(g: OracleGeometry, b: np.ndarray, n_iter: int, lam: float = 1.0,
             if nonneg:
                 x = np.maximum(x, 0.0)
     return x
+
+
+def mlem(g: OracleGeometry, b: np.ndarray, n_iter: int, block: int | None = None,
+         x0: np.ndarray | None = None) -> np.ndarray:
+    """MLEM / OS-EM (Shepp & Vardi, cited at P:266; reading c-I4), step by step: for each
+    iteration and subset S,  x <- x * M_S^T(b_S / M_S x) / C_S  with C_S = M_S^T 1; a ray the
+    estimate does not reach (M_S x = 0) contributes 0, a voxel no ray sees (C_S = 0) is kept.
+    x0 defaults to 1 everywhere.  b: [Np][Nv][Nu].  Returns x [Nz][Ny][Nx] fp64."""
+    Np = b.shape[0]
+    block = block or Np
+    x = np.ones((g.Nz, g.Ny, g.Nx)) if x0 is None else np.array(x0, dtype=np.float64)
+    for _ in range(n_iter):
+        for s0 in range(0, Np, block):
+            n = min(block, Np - s0)
+            C = backproject_volume(g, np.ones((n, g.Nv, g.Nu)), s0=s0)
+            ax = forward_project(g, x, s0, n)
+            ratio = np.where(ax > 0, b[s0:s0 + n] / np.where(ax > 0, ax, 1.0), 0.0)
+            c = backproject_volume(g, ratio, s0=s0)
+            x = np.where(C > 0, x * c / np.where(C > 0, C, 1.0), x)
+    return x

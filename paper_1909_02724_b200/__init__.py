@@ -19,8 +19,10 @@ from .ifdk import (  # noqa: F401
     ifdk_reconstruct,
     ifdk_reconstruct_host,
     ifdk_reconstruct_slab_host,
+    ifdk_mlem_ratio,
+    ifdk_mlem_update,
     ifdk_sart_ratio,
     ifdk_sart_update,
     last_launch_count,
 )
-from .iterative import SART, sart  # noqa: F401
+from .iterative import SART, mlem, sart  # noqa: F401

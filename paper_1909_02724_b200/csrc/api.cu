@@ -198,6 +198,30 @@ extern "C" ifdk_status ifdk_sart_update(float* x_dev, const float* c_dev, const 
     return launch_sart_update(x_dev, c_dev, C_dev, lambda, n, nonneg, (cudaStream_t)stream);
 }
 
+extern "C" ifdk_status ifdk_mlem_ratio(const float* b_dev, const float* ax_dev, float* out_dev,
+                                       long n, void* stream)
+{
+    t_launches = 0;
+    if (n < 0) return fail(IFDK_ERR_SHAPE, "n < 0");
+    if (n > 0 && (!b_dev || !ax_dev || !out_dev))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    return launch_mlem_ratio(b_dev, ax_dev, out_dev, n, (cudaStream_t)stream);
+}
+
+extern "C" ifdk_status ifdk_mlem_update(float* x_dev, const float* c_dev, const float* C_dev,
+                                        long n, void* stream)
+{
+    t_launches = 0;
+    if (n < 0) return fail(IFDK_ERR_SHAPE, "n < 0");
+    if (n > 0 && (!x_dev || !c_dev || !C_dev))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    ifdk_status s = need_device();
+    if (s != IFDK_OK) return s;
+    return launch_mlem_update(x_dev, c_dev, C_dev, n, (cudaStream_t)stream);
+}
+
 extern "C" ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream)
 {
     t_launches = 0;

@@ -354,6 +354,27 @@ __global__ void sart_update_kernel(float* x, const float* __restrict__ c,
     }
 }
 
+// MLEM / OS-EM (reading c-I4): ratio b / (M x) where M x > 0 (else 0), and the
+// multiplicative update x <- x c / C where C = M^T 1 > 0 (else x unchanged).
+__global__ void mlem_ratio_kernel(const float* __restrict__ b, const float* ax, float* out, long n)
+{
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n;
+         e += (long)gridDim.x * blockDim.x) {
+        const float a = ax[e];
+        out[e] = a > 0.f ? b[e] / a : 0.f;
+    }
+}
+
+__global__ void mlem_update_kernel(float* x, const float* __restrict__ c,
+                                   const float* __restrict__ C, long n)
+{
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n;
+         e += (long)gridDim.x * blockDim.x) {
+        const float w = C[e];
+        if (w > 0.f) x[e] = x[e] * c[e] / w;
+    }
+}
+
 __global__ void fill_kernel(float* x, float value, long n)
 {
     for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < n;
@@ -390,6 +411,27 @@ ifdk_status launch_sart_update(float* x, const float* c, const float* C, float l
     sart_update_kernel<<<elementwise_grid(n), 256, 0, st>>>(x, c, C, lam, n, nonneg);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "sart_update_kernel launch");
+    count_launch();
+    return IFDK_OK;
+}
+
+ifdk_status launch_mlem_ratio(const float* b, const float* ax, float* out, long n,
+                              cudaStream_t st)
+{
+    if (n == 0) return IFDK_OK;
+    mlem_ratio_kernel<<<elementwise_grid(n), 256, 0, st>>>(b, ax, out, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "mlem_ratio_kernel launch");
+    count_launch();
+    return IFDK_OK;
+}
+
+ifdk_status launch_mlem_update(float* x, const float* c, const float* C, long n, cudaStream_t st)
+{
+    if (n == 0) return IFDK_OK;
+    mlem_update_kernel<<<elementwise_grid(n), 256, 0, st>>>(x, c, C, n);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "mlem_update_kernel launch");
     count_launch();
     return IFDK_OK;
 }

@@ -73,6 +73,9 @@ ifdk_status launch_sart_ratio(const float* b, const float* ax, const float* R, f
                               cudaStream_t st);
 ifdk_status launch_sart_update(float* x, const float* c, const float* C, float lam, long n,
                                int nonneg, cudaStream_t st);
+ifdk_status launch_mlem_ratio(const float* b, const float* ax, float* out, long n,
+                              cudaStream_t st);
+ifdk_status launch_mlem_update(float* x, const float* c, const float* C, long n, cudaStream_t st);
 ifdk_status launch_fill(float* x, float value, long n, cudaStream_t st);
 
 // baseline.cu (measured baselines, not the production path)

@@ -44,6 +44,8 @@ EXPORTS = (
     "ifdk_forward_project",
     "ifdk_sart_ratio",
     "ifdk_sart_update",
+    "ifdk_mlem_ratio",
+    "ifdk_mlem_update",
     "ifdk_fill",
     "ifdk_last_launch_count",
     "ifdk_last_error",
@@ -97,6 +99,10 @@ _lib.ifdk_sart_ratio.argtypes = [_vp, _vp, _vp, _vp, _l, _vp]
 _lib.ifdk_sart_ratio.restype = _i
 _lib.ifdk_sart_update.argtypes = [_vp, _vp, _vp, ctypes.c_float, _l, _i, _vp]
 _lib.ifdk_sart_update.restype = _i
+_lib.ifdk_mlem_ratio.argtypes = [_vp, _vp, _vp, _l, _vp]
+_lib.ifdk_mlem_ratio.restype = _i
+_lib.ifdk_mlem_update.argtypes = [_vp, _vp, _vp, _l, _vp]
+_lib.ifdk_mlem_update.restype = _i
 _lib.ifdk_fill.argtypes = [_vp, ctypes.c_float, _l, _vp]
 _lib.ifdk_fill.restype = _i
 _lib.ifdk_last_launch_count.argtypes = []
@@ -314,6 +320,24 @@ def ifdk_sart_update(x, c, C, lam: float, nonneg: bool = False, stream=None) -> 
         raise ValueError("x, c and C must have the same size")
     _check(_lib.ifdk_sart_update(_dev_f32(x, "x"), _dev_f32(c, "c"), _dev_f32(C, "C"),
                                  float(lam), n, 1 if nonneg else 0, _stream_ptr(stream)))
+
+
+def ifdk_mlem_ratio(b, ax, out, stream=None) -> None:
+    """out = b / ax where ax > 0, else 0; equal-size float32 CUDA tensors."""
+    n = b.numel()
+    if not (ax.numel() == out.numel() == n):
+        raise ValueError("b, ax and out must have the same size")
+    _check(_lib.ifdk_mlem_ratio(_dev_f32(b, "b"), _dev_f32(ax, "ax"), _dev_f32(out, "out"), n,
+                                _stream_ptr(stream)))
+
+
+def ifdk_mlem_update(x, c, C, stream=None) -> None:
+    """x = x c / C where C > 0 (else unchanged)."""
+    n = x.numel()
+    if not (c.numel() == C.numel() == n):
+        raise ValueError("x, c and C must have the same size")
+    _check(_lib.ifdk_mlem_update(_dev_f32(x, "x"), _dev_f32(c, "c"), _dev_f32(C, "C"), n,
+                                 _stream_ptr(stream)))
 
 
 def ifdk_fill(x, value: float, stream=None) -> None:

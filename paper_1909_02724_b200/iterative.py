@@ -10,7 +10,9 @@ consecutive views:
     x <- x + lam * M_S^T((b_S - M_S x) / R_S) / C_S,   R_S = M_S 1,  C_S = M_S^T 1,
 
 terms with a zero normaliser left out (reading c-I3).  One subset holding every view is
-SIRT.  Every arithmetic step runs in libifdk kernels; torch only allocates the buffers.
+SIRT.  MLEM / OS-EM (Shepp & Vardi, also cited at P:266; reading c-I4) uses the same two
+operators with the multiplicative update  x <- x * M_S^T(b_S / M_S x) / C_S.  Every arithmetic
+step runs in libifdk kernels; torch only allocates the buffers.
 """
 from __future__ import annotations
 
@@ -19,6 +21,8 @@ from .ifdk import (
     ifdk_backproject,
     ifdk_fill,
     ifdk_forward_project,
+    ifdk_mlem_ratio,
+    ifdk_mlem_update,
     ifdk_sart_ratio,
     ifdk_sart_update,
 )
@@ -85,3 +89,36 @@ def sart(g: Geometry, b, n_iter: int, lam: float = 1.0, block: int | None = None
     else:
         x.copy_(x0)
     return SART(g, b, block).iterate(x, n_iter, lam, nonneg)
+
+
+def mlem(g: Geometry, b, n_iter: int, block: int | None = None, x0=None):
+    """MLEM (block=None) or OS-EM (block views per subset) from x0 (default 1 everywhere):
+    x <- x * M_S^T(b_S / M_S x) / M_S^T 1 per subset (reading c-I4)."""
+    import torch
+
+    Np = b.shape[0]
+    block = block or Np
+    subsets = [(s0, min(block, Np - s0)) for s0 in range(0, Np, block)]
+    dev = b.device
+    x = torch.empty((g.Nz, g.Ny, g.Nx), device=dev)
+    if x0 is None:
+        ifdk_fill(x, 1.0)
+    else:
+        x.copy_(x0)
+    ax = torch.empty((block, g.Nv, g.Nu), device=dev)
+    c = torch.empty_like(x)
+    ones_proj = torch.empty((block, g.Nv, g.Nu), device=dev)
+    ifdk_fill(ones_proj, 1.0)
+    C = []
+    for s0, n in subsets:
+        Cq = torch.empty_like(x)
+        ifdk_backproject(g, ones_proj[:n], s0, Cq)
+        C.append(Cq)
+    for _ in range(n_iter):
+        for q, (s0, n) in enumerate(subsets):
+            a = ax[:n]
+            ifdk_forward_project(g, x, s0, a)              # M_S x
+            ifdk_mlem_ratio(b[s0:s0 + n], a, a)            # b / M_S x
+            ifdk_backproject(g, a, s0, c)                  # M_S^T (...)
+            ifdk_mlem_update(x, c, C[q])                   # x * c / C
+    return x

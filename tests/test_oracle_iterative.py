@@ -1,8 +1,9 @@
 """Pins of the iterative-reconstruction oracle (DESIGN.md readings
-c-I1..c-I3): the matched forward projector and SART / SIRT, checked against what the
+c-I1..c-I4): the matched forward projector, SART / SIRT and MLEM / OS-EM, checked against what the
 mathematics fixes -- the adjoint identity with the (independently pinned) back-projector,
 a brute-force ray construction of every splat, closed forms on the rotation axis and
-Eq. equ:z, and the exact one-step solution of a single-voxel system."""
+Eq. equ:z, the exact one-step solution of a single-voxel system, and the monotone decrease
+of SIRT's weighted residual and of MLEM's Kullback-Leibler divergence."""
 import math
 
 import numpy as np
@@ -132,3 +133,39 @@ def test_sirt_weighted_residual_decreases_monotonically():
         prev = cur
     xo = oracle.sart(g, b, 10, lam=1.0, block=3)
     assert wres(xo) < 1e-3 * wres(np.zeros_like(xo))
+
+
+def test_mlem_single_voxel_exact_in_one_step():
+    """One voxel: x1 = x0 / sum a * sum_i a_i b_i / (a_i x0) = sum b / sum a, which is x_true for
+    consistent data, from any positive start (reading c-I4)."""
+    g = OracleGeometry(7, 6, 1, 1, 1, 1.0, 1.0, 1.0, 1.0, 1.0, 40.0, 20.0, 0.7)
+    b = oracle.forward_project(g, np.full((1, 1, 1), 2.5), 0, 5)
+    for x0 in (1.0, 0.3):
+        x = oracle.mlem(g, b, 1, x0=np.full((1, 1, 1), x0))
+        assert abs(x[0, 0, 0] - 2.5) < 1e-13
+
+
+def test_mlem_keeps_positivity_and_decreases_kl():
+    """MLEM on consistent non-negative data keeps the estimate positive and decreases the
+    Kullback-Leibler divergence KL(b || M x) = sum b log(b / Mx) - b + Mx monotonically
+    (the EM property); OS-EM reaches a small divergence."""
+    rng = np.random.default_rng(9)
+    g = OracleGeometry(16, 12, 6, 6, 5, 1.0, 1.0, 1.0, 1.0, 1.0, 50.0, 25.0, 2 * math.pi / 12)
+    x_true = rng.uniform(0.2, 1, (5, 6, 6))
+    b = oracle.forward_project(g, x_true, 0, 12)
+
+    def kl(x):
+        ax = oracle.forward_project(g, x, 0, 12)
+        m = b > 0
+        return float(np.sum(b[m] * np.log(b[m] / ax[m])) - b.sum() + ax.sum())
+
+    x = np.ones((5, 6, 6))
+    prev = kl(x)
+    for _ in range(6):
+        x = oracle.mlem(g, b, 1, x0=x)
+        assert x.min() > 0
+        cur = kl(x)
+        assert cur < prev
+        prev = cur
+    xo = oracle.mlem(g, b, 10, block=3)
+    assert kl(xo) < 1e-2 * kl(np.ones((5, 6, 6)))
