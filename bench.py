@@ -8,9 +8,18 @@ synthetic Shepp-Logan projections (BASELINE.json configs; default config 4:
 2048 projections of 2048^2 -> 2048^3, which fits one GPU).  The metric is GUPS
 (N_x N_y N_z N_p / (T 2^30)) for the whole step plus its end-to-end
 seconds.  N > 1 runs the k-slab split (dist.kslab_reconstruct) under torchrun:
-every rank filters its own views, an NCCL all-to-all moves row bands, each rank
-back-projects its slab; the step time is the max over ranks (CUDA events + barrier).
-`--impl reference` times the fp64 CPU oracle (oracle/) on a bounded sample.
+every rank filters its own views, the filter stores each row band straight into the
+ranks that need it (symmetric memory over NVLink; `--exchange nccl`: an NCCL
+all-to-all), each rank back-projects its slab; the step time is the max over ranks
+(CUDA events + barrier).  `--impl reference` times the fp64 CPU oracle (oracle/) on a
+bounded sample.
+
+Besides the contract keys the line carries: `roofline` (BP against the measured
+shared-memory gather peak, with ncu DRAM traffic), `roofline_hbm`, `roofline_issue`,
+`filter_roofline`, `e2e` through the C ABI with its `host_legs`, `cpu_baseline` (oracle),
+`other_configs` (configs 1-3 and config 5's per-rank slab at N = 1), `iterative` (one
+config-3 SIRT iteration and the forward projector) and, at N > 1, `stage_ms` and
+`variants` (projection split, R x C grid).
 """
 from __future__ import annotations
 
