@@ -177,3 +177,20 @@ def test_band_exchange_volume_config4_p8():
         rows += sum(ex.views[r][1] * (hi - lo + 1) for r, (lo, hi) in enumerate(ex.recv))
     full = spec.Np * spec.Nv
     assert rows / full < 0.2, rows / full
+
+
+def test_d2h_pieces_cover_the_slab_on_chunk_boundaries():
+    """The end-to-end driver's D2H pieces tile the slab exactly, start on multiples of 64
+    slices relative to the slab start (the BP chunk, so sub-slab launches leave the result
+    unchanged) and end with pieces of at most D2H_TAIL slices."""
+    from paper_1909_02724_b200.dist import D2H_SUBSLAB, D2H_TAIL, _d2h_pieces
+
+    for k0, nk in ((0, 2048), (256, 256), (0, 100), (64, 600), (512, 513), (0, 1)):
+        pieces = _d2h_pieces(k0, nk)
+        a = k0
+        for s, n in pieces:
+            assert s == a and 0 < n <= D2H_SUBSLAB and (s - k0) % 64 == 0
+            a += n
+        assert a == k0 + nk
+        tail = [n for s, n in pieces if s >= k0 + nk - D2H_SUBSLAB]
+        assert all(n <= D2H_TAIL for n in tail)
