@@ -356,10 +356,12 @@ static ifdk_status reconstruct_host_impl(const ifdk_geometry* g, const float* ra
             const long nb = bat[b].second;
             if (b >= 2) cudaStreamWaitEvent(cp, consumed[q], 0);
             // rows v0..v0+n_rows-1 of views b0..b0+nb-1: one 2-D copy (a contiguous run per view)
-            cudaMemcpy2DAsync(buf[q], sizeof(float) * view_elems,
-                              raw_host + b0 * host_view_elems + (size_t)v0 * g->Nu,
-                              sizeof(float) * host_view_elems, sizeof(float) * view_elems, nb,
-                              cudaMemcpyHostToDevice, cp);
+            const cudaError_t ce =
+                cudaMemcpy2DAsync(buf[q], sizeof(float) * view_elems,
+                                  raw_host + b0 * host_view_elems + (size_t)v0 * g->Nu,
+                                  sizeof(float) * host_view_elems, sizeof(float) * view_elems, nb,
+                                  cudaMemcpyHostToDevice, cp);
+            if (ce != cudaSuccess && s == IFDK_OK) s = cuda_fail(ce, "cudaMemcpy2DAsync(views H2D)");
             cudaEventRecord(copied[q], cp);
         };
         if (nbatches > 0) enqueue_copy(0);
