@@ -183,13 +183,13 @@ def test_bp_slab_split_is_bitwise_and_deterministic(torch_cuda):
             assert torch.equal(slab, full[a:b]), (cuts, a, b)
 
 
-@pytest.mark.parametrize("walk", ["2", "3", "5"])
-def test_bp_walk_variants(torch_cuda, monkeypatch, walk):
-    """The default PAIR walk on packed fp32x2 instructions (WALK 4) gives bitwise the values of
-    the scalar PAIR walk (WALK 2: the same operations and roundings, element by element) and
-    of the RAW-staged walk (WALK 5: b - a formed in registers instead of in a rewritten patch),
-    on whole chunks and on partial ones (slab cut inside a chunk); the TRIPLE walk (WALK 3)
-    matches the oracle."""
+def test_bp_walk_variants(torch_cuda, monkeypatch):
+    """PAIR walks: the fp32x2 walk on the pair patch (WALK 4), the scalar walk (2) and the RAW
+    walk reading the TMA box (5) are bitwise equal, on whole chunks and on partial ones (slab
+    cut inside a chunk).  TRIPLE walks: the RAW triple walk (6, the default where
+    0.5 <= dv/dk) and the scalar triple walk on the pair patch (3, which serves walk 6's
+    partial chunks) are bitwise equal, a slab split under walk 6 is bitwise the whole-volume
+    result, and both match the oracle."""
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_backproject
 
@@ -205,16 +205,18 @@ def test_bp_walk_variants(torch_cuda, monkeypatch, walk):
         torch.cuda.synchronize()
         return vol
 
-    x2 = run("4")
-    other = run(walk)
-    if walk in ("2", "5"):  # scalar PAIR walk; RAW staging (taps straight from the TMA box)
-        assert torch.equal(x2, other)
-        assert torch.equal(run("4", 77, 54), run(walk, 77, 54))
-    else:
-        og = oracle.OracleGeometry(**spec.geometry_args())
-        ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
-        assert_parity(other.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp triple walk")
-        assert_parity(x2.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp x2 walk")
+    for walk in ("2", "5"):
+        assert torch.equal(run("4"), run(walk)), walk
+        assert torch.equal(run("4", 77, 54), run(walk, 77, 54)), walk
+    tri = run("6")
+    assert torch.equal(tri, run("3"))
+    assert torch.equal(run("6", 77, 54), run("3", 77, 54))
+    for a, b in ((0, 77), (77, 131), (131, 160)):  # partial chunks at every cut
+        assert torch.equal(run("6", a, b - a), tri[a:b]), (a, b)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
+    assert_parity(tri.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp triple walk")
+    assert_parity(run("4").cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp pair walk")
 
 
 def test_bp_view_split_accumulate_matches(torch_cuda):
