@@ -205,6 +205,59 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
             if (FULL || (kk + 1 >= kv0 && kk + 1 < kv1))
                 acc[kk + 1] = fmaf(t.W, fmaf(g, d, h1), acc[kk + 1]);
         }
+    } else if constexpr (WALK == 8) {
+        // 3-ROW TRIPLE (needs dv < 1/2, config 5): slices kk, kk+1, kk+2 all lie within rows
+        // n .. n+2 (fr + 2 dv < 2); slices kk+1 and kk+2 sit g1 = fr + dv - 1 and g2 = g1 + dv
+        // rows past row n+1 (both in [-1, 1)).  Same grouping and pair tail as the RAW form
+        // (walk 7), which it serves on partial chunks, bitwise.
+        constexpr int TRI_END = KC - 4;
+        static_assert(TRI_END % 3 == 0, "whole triples before the pair tail");
+#pragma unroll
+        for (int kk = 0; kk + 3 <= TRI_END; kk += 3) {
+            if (kk == 0 || (kk >> 3) != ((kk - 3) >> 3)) {
+                hook(kk >> 3);
+                asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
+            }
+            float fr0;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
+            const uint32_t addr = bits * S + a0;
+            const float2 p0 = lds64(addr);
+            const float2 p1 = lds64(addr + S);
+            const float2 p2 = lds64(addr + 2 * S);
+            const float h0 = fmaf(t.du, p0.y, p0.x);  // Alg. alg:subpixel lines 4-5
+            const float h1 = fmaf(t.du, p1.y, p1.x);
+            const float h2 = fmaf(t.du, p2.y, p2.x);
+            const float d01 = h1 - h0, d12 = h2 - h1;
+            if (FULL || (kk >= kv0 && kk < kv1))
+                acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);  // line 6; Alg. alg:bp line 10
+            const float g1 = fr0 + t.dvm1;
+            const float e1 = g1 >= 0.f ? d12 : d01;
+            if (FULL || (kk + 1 >= kv0 && kk + 1 < kv1))
+                acc[kk + 1] = fmaf(t.W, fmaf(g1, e1, h1), acc[kk + 1]);
+            const float g2 = g1 + t.dv;
+            const float e2 = g2 >= 0.f ? d12 : d01;
+            if (FULL || (kk + 2 >= kv0 && kk + 2 < kv1))
+                acc[kk + 2] = fmaf(t.W, fmaf(g2, e2, h1), acc[kk + 2]);
+        }
+#pragma unroll
+        for (int kk = TRI_END; kk < KC; kk += 2) {  // the PAIR tail
+            float fr0;
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
+            const uint32_t addr = bits * S + a0;
+            const float2 p0 = lds64(addr);
+            const float2 p1 = lds64(addr + S);
+            const float2 p2 = lds64(addr + 2 * S);
+            const float h0 = fmaf(t.du, p0.y, p0.x);
+            const float h1 = fmaf(t.du, p1.y, p1.x);
+            const float h2 = fmaf(t.du, p2.y, p2.x);
+            const float d01 = h1 - h0;
+            if (FULL || (kk >= kv0 && kk < kv1))
+                acc[kk] = fmaf(t.W, fmaf(fr0, d01, h0), acc[kk]);
+            const float g = fr0 + t.dvm1;
+            const float d = g >= 0.f ? h2 - h1 : d01;
+            if (FULL || (kk + 1 >= kv0 && kk + 1 < kv1))
+                acc[kk + 1] = fmaf(t.W, fmaf(g, d, h1), acc[kk + 1]);
+        }
     } else if constexpr (WALK == 2) {
 #pragma unroll
         for (int kk = 0; kk < KC; kk += 2) {
@@ -477,7 +530,7 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
     if constexpr (WALK == 2 || WALK == 4) {
         ka = kv0 & ~1;
         kz = (kv1 - 1) | 1;
-    } else if constexpr (WALK == 3) {  // triples start on multiples of 3; the tail is pairs
+    } else if constexpr (WALK == 3 || WALK == 8) {  // triples on multiples of 3; pair tail
         constexpr int TRI_END = KC - 4;
         ka = kv0 < TRI_END ? kv0 - kv0 % 3 : (kv0 & ~1);
         kz = (kv1 - 1) < TRI_END ? (kv1 - 1) / 3 * 3 + 2 : ((kv1 - 1) | 1);
@@ -786,7 +839,7 @@ __device__ __forceinline__ void accumulate_view_raw_x2(f2x (&acc)[KC / 2], uint3
 // fp32x2 halves: 16 LDS.32 per 6 updates (10.7 B/update of shared memory instead of 12).  The
 // first 60 slices run as ten such groups, the last 4 as one PAIR quad.  Accumulator pairs:
 // acc[3 q + r] = (slice 6 q + r, slice 6 q + 3 + r) for r < 3, acc[30 + r] = (60 + r, 62 + r).
-template <int KC, int BW>
+template <int KC, int BW, bool ROWS3>
 __device__ __forceinline__ void accumulate_view_raw_x2_triple(f2x (&acc)[KC / 2],
                                                               uint32_t raw_base,
                                                               uint32_t neg_magic,
@@ -809,21 +862,30 @@ __device__ __forceinline__ void accumulate_view_raw_x2_triple(f2x (&acc)[KC / 2]
         const f2x fr = sub2(v, add2(tb, nmagic2));
         const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
         const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
-        f2x h[4];
+        constexpr int NR = ROWS3 ? 3 : 4;
+        f2x h[NR];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < NR; ++r) {
             const f2x a = pk2(lds32(adA + r * S), lds32(adB + r * S));
             const f2x b = pk2(lds32(adA + r * S + 4), lds32(adB + r * S + 4));
             h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
         }
-        const f2x d01 = sub2(h[1], h[0]), d12 = sub2(h[2], h[1]), d23 = sub2(h[3], h[2]);
+        const f2x d01 = sub2(h[1], h[0]), d12 = sub2(h[2], h[1]);
         const f2x g1 = add2(fr, dvm12);   // second slice: g1 rows past row n+1, in [-1, 1)
-        const f2x g2 = add2(g1, dvm12);   // third slice: g2 rows past row n+2, in [-1, 1)
         const f2x e1 = pk2(lo2(g1) >= 0.f ? lo2(d12) : lo2(d01), hi2(g1) >= 0.f ? hi2(d12) : hi2(d01));
-        const f2x e2 = pk2(lo2(g2) >= 0.f ? lo2(d23) : lo2(d12), hi2(g2) >= 0.f ? hi2(d23) : hi2(d12));
         acc[3 * q] = fma2(W2, fma2(fr, d01, h[0]), acc[3 * q]);      // line 6; Alg. alg:bp line 10
         acc[3 * q + 1] = fma2(W2, fma2(g1, e1, h[1]), acc[3 * q + 1]);
-        acc[3 * q + 2] = fma2(W2, fma2(g2, e2, h[2]), acc[3 * q + 2]);
+        if constexpr (ROWS3) {
+            // dv < 1/2: the third slice sits g2 = g1 + dv rows past row n+1, still in rows n..n+2
+            const f2x g2 = add2(g1, dv2);
+            const f2x e2 = pk2(lo2(g2) >= 0.f ? lo2(d12) : lo2(d01), hi2(g2) >= 0.f ? hi2(d12) : hi2(d01));
+            acc[3 * q + 2] = fma2(W2, fma2(g2, e2, h[1]), acc[3 * q + 2]);
+        } else {
+            const f2x d23 = sub2(h[NR - 1], h[2]);
+            const f2x g2 = add2(g1, dvm12);   // third slice: g2 rows past row n+2, in [-1, 1)
+            const f2x e2 = pk2(lo2(g2) >= 0.f ? lo2(d23) : lo2(d12), hi2(g2) >= 0.f ? hi2(d23) : hi2(d12));
+            acc[3 * q + 2] = fma2(W2, fma2(g2, e2, h[2]), acc[3 * q + 2]);
+        }
         if (q & 1)
             asm volatile("" : "+l"(acc[3 * q - 3]), "+l"(acc[3 * q - 2]), "+l"(acc[3 * q - 1]),
                          "+l"(acc[3 * q]), "+l"(acc[3 * q + 1]), "+l"(acc[3 * q + 2]));
@@ -877,7 +939,7 @@ __device__ __forceinline__ void flush_x2_triple(f2x (&acc)[KC / 2], const BPPara
 
 constexpr int kRawBuf = 4;  // TMA boxes in flight / in use per CTA
 
-template <int KC, int BW, bool TRI = false>
+template <int KC, int BW, int TRI = 0>  // 0: PAIR walk, 1: 4-row TRIPLE, 2: 3-row TRIPLE
 __global__ void __launch_bounds__(kThreads, 2)
     bp_raw_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
                   const __grid_constant__ PTable pt)
@@ -952,8 +1014,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int b = t % kRawBuf;
         mbar_wait(&mbar[b], (uint32_t)((t / kRawBuf) & 1));
         const uint32_t rb = raw0 + (uint32_t)(b * p.raw_bytes);
-        if constexpr (TRI)
-            accumulate_view_raw_x2_triple<KC, BW>(acc, rb, p.neg_magic, ti, u_org, v_org);
+        if constexpr (TRI != 0)
+            accumulate_view_raw_x2_triple<KC, BW, TRI == 2>(acc, rb, p.neg_magic, ti, u_org, v_org);
         else
             accumulate_view_raw_x2<KC, BW>(acc, rb, p.neg_magic, ti, u_org, v_org);
         if ((t >= first_flush && (t - first_flush) % p.vb == 0) || t == n - 1) {
@@ -962,7 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
             const bool ow = !p.accumulate && t <= first_flush;
             if (fi < p.Nx && fj < p.Ny) {
-                if constexpr (TRI)
+                if constexpr (TRI != 0)
                     flush_x2_triple<KC>(acc, p, fi, fj, kb, ow);
                 else
                     flush_x2<KC>(acc, p, fi, fj, kb, 0, KC, ow);
@@ -1032,12 +1094,15 @@ int choose_walk(const ifdk_geometry* g)
 {
     if (!use_pair(g)) return 1;
     const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
-    // TRIPLE RAW walk where 0.5 <= dv/dk (configs 1-4): 2000 vs 1884 GUPS (config 4, 256 views)
-    int w = dv_min >= 0.5001 ? 6 : kDefaultPairWalk;
+    // TRIPLE RAW walks: 4-row where 0.5 <= dv/dk (configs 1-4: 2000 vs 1884 GUPS on config 4),
+    // 3-row where dv/dk < 0.5 everywhere (config 5)
+    const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
+    int w = dv_min >= 0.5001 ? 6 : dv_max < 0.4999 ? 7 : kDefaultPairWalk;
     if (const char* e = std::getenv("IFDK_BP_WALK")) {
         const int v = std::atoi(e);
         if (v == 2 || v == 4 || v == 5) w = v;
-        if (v == 6 && dv_min >= 0.5001) w = 6;  // TRIPLE RAW walk (configs 1-4)
+        if (v == 6 && dv_min >= 0.5001) w = 6;  // 4-row TRIPLE RAW walk (configs 1-4)
+        if ((v == 7 || v == 8) && dv_max < 0.4999) w = v;  // 3-row TRIPLE (RAW / pair patch)
         if (v == 3 && dv_min >= 0.5001) w = 3;
     }
     return w;
@@ -1112,7 +1177,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         int box_w = box_w0, P2 = 0, BW = 0;
         for (int c : {24, 40, 56, 72})
             if (c >= box_w - 1) { P2 = c; break; }
-        if (w == 5 || w == 6) {
+        if (w == 5 || w == 6 || w == 7) {
             for (int c : {40, 72})  // row pitch = 8 mod 32 words: conflict-free LDS.32 taps
                 if (c >= box_w) { BW = c; break; }
             box_w = BW;
@@ -1149,8 +1214,9 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         dim3 grid((unsigned)(q.raster * tiles_j), (unsigned)nch,
                   (unsigned)((q.tiles_i + q.raster - 1) / q.raster));
         if (BW) {
-            auto k = w == 6 ? (BW == 40 ? bp_raw_kernel<64, 40, true> : bp_raw_kernel<64, 72, true>)
-                            : (BW == 40 ? bp_raw_kernel<64, 40> : bp_raw_kernel<64, 72>);
+            auto k = w == 6   ? (BW == 40 ? bp_raw_kernel<64, 40, 1> : bp_raw_kernel<64, 72, 1>)
+                     : w == 7 ? (BW == 40 ? bp_raw_kernel<64, 40, 2> : bp_raw_kernel<64, 72, 2>)
+                              : (BW == 40 ? bp_raw_kernel<64, 40> : bp_raw_kernel<64, 72>);
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp raw)");
@@ -1160,7 +1226,17 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             count_launch();
             return IFDK_OK;
         }
-        if (w == 5 || w == 6) w = 4;
+        if (w == 5) w = 4;
+        if (w == 6) w = 3;
+        if (w == 7) w = 8;
+        if (w == 8) {
+            switch (P2) {
+                case 24: return launch_t<64, 24, 8>(q, map, pt, tma, grid, smem, st);
+                case 40: return launch_t<64, 40, 8>(q, map, pt, tma, grid, smem, st);
+                case 56: return launch_t<64, 56, 8>(q, map, pt, tma, grid, smem, st);
+                default: return launch_t<64, 72, 8>(q, map, pt, tma, grid, smem, st);
+            }
+        }
         if (w == 3) {
             switch (P2) {
                 case 24: return launch_t<64, 24, 3>(q, map, pt, tma, grid, smem, st);
@@ -1198,15 +1274,16 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         }
     };
 
-    if ((walk != 5 && walk != 6) || !tma_ok || box_w0 > 72) return run(walk, p.kb0, n_chunks);
+    if ((walk != 5 && walk != 6 && walk != 7) || !tma_ok || box_w0 > 72)
+        return run(walk, p.kb0, n_chunks);
     // RAW staging runs the whole chunks; a partial chunk at either slab end (its masked slices
     // would read rows outside the box) takes the x2 pair walk, bitwise the same values.
     const bool head = (k0 % KC) != 0, tail = ((k0 + nk) % KC) != 0;
     const int c0 = head ? 1 : 0, c1 = tail ? n_chunks - 1 : n_chunks;
     ifdk_status s = IFDK_OK;
     if (c1 > c0) s = run(walk, p.kb0 + c0 * KC, c1 - c0);
-    // partial chunks: walk 4 for walk 5, walk 3 for walk 6 (bitwise the same arithmetic)
-    const int wp = walk == 6 ? 3 : 4;
+    // partial chunks: walk 4 for walk 5, 3 for 6, 8 for 7 (bitwise the same arithmetic)
+    const int wp = walk == 6 ? 3 : walk == 7 ? 8 : 4;
     if (s == IFDK_OK && head) s = run(wp, p.kb0, 1);
     if (s == IFDK_OK && tail && (n_chunks - 1 > 0 || !head)) s = run(wp, p.kb0 + (n_chunks - 1) * KC, 1);
     return s;

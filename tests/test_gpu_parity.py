@@ -219,6 +219,35 @@ def test_bp_walk_variants(torch_cuda, monkeypatch):
     assert_parity(run("4").cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp pair walk")
 
 
+def test_bp_three_row_triple_walk(torch_cuda, monkeypatch):
+    """dv/dk < 1/2 (config 5's regime): the 3-row TRIPLE RAW walk (7, the default there) and its
+    pair-patch companion (8, partial chunks) are bitwise equal, slab splits are bitwise the
+    whole-volume result, and the result matches the oracle."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+
+    spec = _spec(48, 96, 96, 48, 40, 200)  # dv/dk in [0.29, 0.37]
+    g = Geometry.from_spec(spec)
+    Qn = _oracle_Q32(spec, _phantom_E(spec))
+    Q = torch.from_numpy(Qn).cuda()
+
+    def run(w, k0=0, nk=spec.Nz):
+        monkeypatch.setenv("IFDK_BP_WALK", w)
+        vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
+        ifdk_backproject(g, Q, 0, vol, k0=k0)
+        torch.cuda.synchronize()
+        return vol
+
+    tri = run("7")
+    assert torch.equal(tri, run("8"))
+    assert torch.equal(run("7", 77, 54), run("8", 77, 54))
+    for a, b in ((0, 77), (77, 131), (131, 200)):
+        assert torch.equal(run("7", a, b - a), tri[a:b]), (a, b)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
+    assert_parity(tri.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp 3-row triple walk")
+
+
 def test_bp_view_split_accumulate_matches(torch_cuda):
     """Views in two calls (accumulate) vs one call: equal up to fp32 summation order."""
     torch = torch_cuda
