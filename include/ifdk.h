@@ -38,6 +38,8 @@
 #ifndef IFDK_H
 #define IFDK_H
 
+#include <stddef.h>
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -59,7 +61,8 @@ typedef struct ifdk_geometry ifdk_geometry; /* opaque, library-owned */
  * theta (beta_s = s*theta; the paper's theta = 2 pi / N_p).
  * N_p is not a geometry argument: any global view index s is allowed.
  * Errors: INVALID_ARGUMENT if a dimension < 1, a pitch <= 0, D <= d, d <= 0,
- * theta not finite or 0, or out == NULL; DEGENERATE_GEOMETRY if the volume's
+ * theta <= 0 or not finite (the rotation sense is fixed by Mrot,
+ * P:556-570), or out == NULL; DEGENERATE_GEOMETRY if the volume's
  * circumscribed radius in the rotation plane is >= d. */
 ifdk_status ifdk_geometry_create(int Nu, int Nv, int Nx, int Ny, int Nz, double Du, double Dv,
                                  double Dx, double Dy, double Dz, double D, double d,
@@ -101,13 +104,52 @@ typedef struct {
  * row-band exchange of the k-slab split: instead of one output array,
  * each filtered row is stored straight into every destination band that contains
  * it (n_dest <= 16; dests is a host array, copied at launch).  With peer-mapped
- * bases the NVLink transfer of a row overlaps the filtering of the next ones; the
- * caller orders the destinations' later reads (e.g. a cross-GPU barrier).
+ * bases (ifdk_peer_open) the NVLink transfer of a row overlaps the filtering of the
+ * next ones.
+ * Completion signal (n_flags > 0): flags is a host array of n_flags <= 16 device
+ * pointers (words in local or peer-mapped memory); once every row of this launch has
+ * been stored, each word is incremented by 1 with a system-scope atomic that is
+ * ordered after all those stores (__threadfence_system by every thread, then the
+ * "last block" ticket; see csrc/peer.cu).  ticket_dev is a caller-owned device word
+ * that must be 0 at launch; the kernel leaves it 0 (launches sharing a ticket must be
+ * stream-ordered).  With n_views == 0 the flags are still incremented.  n_flags = 0:
+ * no signal (flags, ticket_dev may be NULL); the caller then orders the
+ * destinations' later reads itself.
  * Errors: INVALID_ARGUMENT (NULL pointers, n_dest < 1 or > 16, a band outside
- * [0, Nv) or empty), SHAPE (rows outside [0, Nv), n_views < 0). */
+ * [0, Nv) or empty, n_flags outside 0..16, a NULL flag or ticket), SHAPE (rows
+ * outside [0, Nv), n_views < 0). */
 ifdk_status ifdk_filter_scatter(const ifdk_geometry* g, const float* raw_dev, long n_views,
                                 int v0, int n_rows, int n_dest, const ifdk_band_dest* dests,
+                                int n_flags, unsigned int* const* flags, unsigned int* ticket_dev,
                                 void* stream);
+
+/* ---- peer memory and device-side signals of the fused exchange (csrc/peer.cu) ---- */
+
+/* cudaMalloc of `bytes` (a whole allocation, so its IPC handle maps offset 0) and its
+ * 64-byte CUDA IPC handle, to be sent to the other ranks (one process per GPU).
+ * Free with ifdk_peer_free.  Errors: INVALID_ARGUMENT (NULL, 0 bytes), CUDA,
+ * OUT_OF_MEMORY. */
+ifdk_status ifdk_peer_alloc(size_t bytes, void** dev_ptr, unsigned char handle[64]);
+
+/* Map another process's ifdk_peer_alloc buffer into this one (cudaIpcOpenMemHandle
+ * with lazy peer access: NVLink P2P between GPUs, or the same GPU).  *dev_ptr is valid
+ * on the current device until ifdk_peer_close.  Errors: INVALID_ARGUMENT, CUDA. */
+ifdk_status ifdk_peer_open(const unsigned char handle[64], void** dev_ptr);
+ifdk_status ifdk_peer_close(void* dev_ptr);   /* NULL-safe */
+ifdk_status ifdk_peer_free(void* dev_ptr);    /* NULL-safe */
+
+/* After all earlier work on `stream`, increment each of the n_flags <= 16 device words
+ * flags[i] (host array of local or peer-mapped device pointers) by 1 with a
+ * system-scope atomic (used to release a receive buffer once the back-projection that
+ * read it has completed).  Errors: INVALID_ARGUMENT (n_flags outside 0..16, NULL). */
+ifdk_status ifdk_signal(int n_flags, unsigned int* const* flags, void* stream);
+
+/* Later work on `stream` waits until each of the n consecutive device words at
+ * flags_dev (local memory) has reached `target` (compared modulo 2^32, so the
+ * counters may wrap), read with ld.acquire.sys.  A word that never reaches the target
+ * (a dead peer) traps after 300 s instead of hanging the GPU.
+ * Errors: INVALID_ARGUMENT (NULL, n outside 1..1024). */
+ifdk_status ifdk_wait(const unsigned int* flags_dev, int n, unsigned int target, void* stream);
 
 /* Alg. alg:bp + alg:subpixel for views s0..s0+n_views-1 into the
  * slab k0..k0+nk-1:  vol_dev[k-k0][j][i] (=|+=) sum_s f^2 . interp2(Q_s, u, v).
@@ -226,6 +268,15 @@ ifdk_status ifdk_mlem_update(float* x_dev, const float* c_dev, const float* C_de
 /* x[e] = value for n fp32 device elements (normaliser inputs of SART).
  * Errors: INVALID_ARGUMENT (NULL), SHAPE (n < 0). */
 ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream);
+
+/* Speed-tuning hook for A/B measurements and tests, not needed in normal use:
+ * walk selects the back-projection k-walk among the variants that give BITWISE
+ * the same result as the automatic choice for the geometry (PAIR family 2, 4, 5;
+ * 4-row TRIPLE family 3, 6 where 0.5 <= dv/dk; 3-row TRIPLE family 7, 8 where
+ * dv/dk < 0.5); any other value, or 0, means automatic.
+ * raster sets the CTA raster band in tiles (0 = automatic; >= the tile count =
+ * row-major); it only reorders CTAs.  Process-wide; affects later launches. */
+ifdk_status ifdk_set_bp_variant(int walk, int raster);
 
 /* Number of device kernels the last successful call on this thread launched. */
 int ifdk_last_launch_count(void);

@@ -24,5 +24,6 @@ from .ifdk import (  # noqa: F401
     ifdk_sart_ratio,
     ifdk_sart_update,
     last_launch_count,
+    set_bp_variant,
 )
 from .iterative import SART, mlem, sart  # noqa: F401

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libifdk.so")
 PROBE_LIB = os.path.join(HERE, "libifdk_probe.so")  # shared-memory roofline micro-benchmark
-SOURCES = ["geometry.cpp", "filter.cu", "backproject.cu", "forward.cu", "baseline.cu", "api.cu"]
+SOURCES = ["geometry.cpp", "filter.cu", "backproject.cu", "forward.cu", "baseline.cu", "peer.cu",
+           "api.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-lineinfo",
     "-gencode", "arch=compute_100a,code=sm_100a",

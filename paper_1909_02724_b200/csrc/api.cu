@@ -96,12 +96,23 @@ extern "C" ifdk_status ifdk_filter(const ifdk_geometry* g, const float* raw_dev,
 
 extern "C" ifdk_status ifdk_filter_scatter(const ifdk_geometry* g, const float* raw_dev,
                                            long n_views, int v0, int n_rows, int n_dest,
-                                           const ifdk_band_dest* dests, void* stream)
+                                           const ifdk_band_dest* dests, int n_flags,
+                                           unsigned int* const* flags, unsigned int* ticket_dev,
+                                           void* stream)
 {
     t_launches = 0;
     if (!g || !raw_dev || !dests) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
     if (n_dest < 1 || n_dest > kMaxFilterDest)
         return fail(IFDK_ERR_INVALID_ARGUMENT, "n_dest must be 1..16");
+    if (n_flags < 0 || n_flags > kMaxFilterDest || (n_flags > 0 && (!flags || !ticket_dev)))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "need 0 <= n_flags <= 16, flags and a ticket");
+    PeerFlags pf{};
+    pf.n = n_flags;
+    pf.ticket = ticket_dev;
+    for (int f = 0; f < n_flags; ++f) {
+        if (!flags[f]) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL flag");
+        pf.flag[f] = flags[f];
+    }
     for (int d = 0; d < n_dest; ++d)
         if (!dests[d].base || dests[d].v_lo < 0 || dests[d].v_hi >= g->Nv ||
             dests[d].v_hi < dests[d].v_lo)
@@ -110,7 +121,7 @@ extern "C" ifdk_status ifdk_filter_scatter(const ifdk_geometry* g, const float* 
     if (s != IFDK_OK) return s;
     if ((s = need_device()) != IFDK_OK) return s;
     return launch_filter(const_cast<ifdk_geometry*>(g), raw_dev, nullptr, n_views, v0, n_rows,
-                         (cudaStream_t)stream, n_dest, dests);
+                         (cudaStream_t)stream, n_dest, dests, n_flags > 0 ? &pf : nullptr);
 }
 
 extern "C" ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* filtered_dev,
@@ -487,3 +498,10 @@ extern "C" void ifdk_geometry_destroy(ifdk_geometry* g)
 extern "C" int ifdk_last_launch_count(void) { return t_launches; }
 
 extern "C" const char* ifdk_last_error(void) { return t_last_error.c_str(); }
+
+extern "C" ifdk_status ifdk_set_bp_variant(int walk, int raster)
+{
+    if (walk < 0 || raster < 0) return fail(IFDK_ERR_INVALID_ARGUMENT, "walk and raster must be >= 0");
+    set_bp_variant(walk, raster);
+    return IFDK_OK;
+}

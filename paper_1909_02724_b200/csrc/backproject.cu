@@ -25,12 +25,16 @@
 //    the two-level summation, so the split does not change a bit.
 //  * Views are summed in order; every VB views (aligned to global view index) the register
 //    partial sums are added to the volume, a two-level summation.
-//  * A view whose patch does not fit the box (never for the five configs) is accumulated
-//    from global memory with bitwise-identical arithmetic.
+//  * The box is sized from a conservative geometric bound (patch_bound), so every view's
+//    patch fits it; a violation is a bug and traps (it kills the CUDA context).  Geometries
+//    whose box cannot be described to TMA or exceeds the opt-in shared memory (N_u % 4 != 0,
+//    box taller than 256 rows or too large) take the same walk with taps read from global
+//    memory, bitwise-identical arithmetic.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -123,6 +127,19 @@ __device__ __forceinline__ float2 lds64(uint32_t addr)
     return v;
 }
 
+// Partial chunks (FULL = false) run the whole unrolled walk and mask only the accumulation,
+// so the floors of masked slices -- below the first slice of a head chunk, past the last one
+// of a tail chunk -- can point outside the box, which was sized for the slices in the slab
+// only; clamping the floor address into the box keeps every shared load inside the
+// allocation.  Unmasked slices' addresses are inside the box already, so their values do not
+// change.  [lo, hi] = first and last floor address whose NR rows stay in the box.
+template <bool FULL>
+__device__ __forceinline__ uint32_t clamp_floor(uint32_t addr, uint32_t lo, uint32_t hi)
+{
+    if constexpr (FULL) return addr;
+    else return min(max(addr, lo), hi);
+}
+
 // One view from the (a, delta) pair patch in shared memory.
 //
 // PAIR (needs dv < 1 px per slice, true for every config): two consecutive slices kk, kk+1
@@ -138,7 +155,7 @@ template <int KC, int P2, bool FULL, int WALK, typename Hook>
 __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t pair_base,
                                                      uint32_t neg_magic, const ThreadInv& t,
                                                      int u_org, int v_org, int kv0, int kv1,
-                                                     Hook&& hook)
+                                                     uint32_t lo_a, uint32_t hi_a, Hook&& hook)
 {
     // byte address of pair (row nv + n, col nu) = pair_base + ((nv - v_org + n) P2 + nu - u_org) 8
     // neg_magic = -0x4B000000 * P2 * 8 (mod 2^32) arrives as a kernel parameter so that ptxas
@@ -165,7 +182,7 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
             }
             float fr0;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
-            const uint32_t addr = bits * S + a0;
+            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float2 p2 = lds64(addr + 2 * S);
@@ -190,7 +207,7 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
         for (int kk = TRI_END; kk < KC; kk += 2) {  // the PAIR tail (see WALK == 2)
             float fr0;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
-            const uint32_t addr = bits * S + a0;
+            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float2 p2 = lds64(addr + 2 * S);
@@ -220,7 +237,7 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
             }
             float fr0;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
-            const uint32_t addr = bits * S + a0;
+            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float2 p2 = lds64(addr + 2 * S);
@@ -243,7 +260,7 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
         for (int kk = TRI_END; kk < KC; kk += 2) {  // the PAIR tail
             float fr0;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
-            const uint32_t addr = bits * S + a0;
+            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float2 p2 = lds64(addr + 2 * S);
@@ -269,7 +286,7 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
             }
             float fr0;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr0);
-            const uint32_t addr = bits * S + a0;
+            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float2 p2 = lds64(addr + 2 * S);
@@ -296,7 +313,7 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
             if (!FULL && (kk < kv0 || kk >= kv1)) continue;
             float fr;
             const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
-            const uint32_t addr = bits * S + a0;
+            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float h0 = fmaf(t.du, p0.y, p0.x);
@@ -363,7 +380,7 @@ template <int KC, int P2, bool FULL, typename Hook>
 __device__ __forceinline__ void accumulate_view_smem_x2(f2x (&acc)[KC / 2], uint32_t pair_base,
                                                         uint32_t neg_magic, const ThreadInv& t,
                                                         int u_org, int v_org, int kv0, int kv1,
-                                                        Hook&& hook)
+                                                        uint32_t lo_a, uint32_t hi_a, Hook&& hook)
 {
     static_assert(KC % 4 == 0, "x2 walk: whole slice quads");
     const uint32_t a0 =
@@ -387,8 +404,8 @@ __device__ __forceinline__ void accumulate_view_smem_x2(f2x (&acc)[KC / 2], uint
         asm("add.rn.f32x2 %0, %0, %1;" : "+l"(kpair) : "l"(four2));
         const f2x tb = add2_rd(v, magic2);
         const f2x fr = sub2(v, add2(tb, nmagic2));
-        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
-        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        const uint32_t adA = clamp_floor<FULL>(__float_as_uint(lo2(tb)) * S + a0, lo_a, hi_a);
+        const uint32_t adB = clamp_floor<FULL>(__float_as_uint(hi2(tb)) * S + a0, lo_a, hi_a);
         const float2 pA0 = lds64(adA), pA1 = lds64(adA + S), pA2 = lds64(adA + 2 * S);
         const float2 pB0 = lds64(adB), pB1 = lds64(adB + S), pB2 = lds64(adB + 2 * S);
         // Alg. alg:subpixel lines 4-5 (horizontal), rows n, n+1, n+2 of A and B
@@ -729,20 +746,24 @@ __global__ void __launch_bounds__(kThreads, KC >= 64 ? 2 : 3)
                 }
             };
             const uint32_t pb = smem_u32(pair0 + (t & 1) * p.box_h * P2);
+            // floor addresses of masked slices are clamped to [pb, hb] (clamp_floor): every
+            // valid floor lies in box rows 1 .. box_h - 3 - pair, and the walk reads at most
+            // 2 + 2 pair rows from its floor
+            const uint32_t hb = pb + (uint32_t)((p.box_h - 2 - p.pair) * P2 * 8 - 8);
             if constexpr (X2) {
                 if (full)
                     accumulate_view_smem_x2<KC, P2, true>(acc.a, pb, p.neg_magic, ti, u_org,
-                                                          v_org, kv0, kv1, row);
+                                                          v_org, kv0, kv1, pb, hb, row);
                 else
                     accumulate_view_smem_x2<KC, P2, false>(acc.a, pb, p.neg_magic, ti, u_org,
-                                                           v_org, kv0, kv1, row);
+                                                           v_org, kv0, kv1, pb, hb, row);
             } else {
                 if (full)
                     accumulate_view_smem<KC, P2, true, WALK>(acc.a, pb, p.neg_magic, ti, u_org,
-                                                             v_org, kv0, kv1, row);
+                                                             v_org, kv0, kv1, pb, hb, row);
                 else
                     accumulate_view_smem<KC, P2, false, WALK>(acc.a, pb, p.neg_magic, ti, u_org,
-                                                              v_org, kv0, kv1, row);
+                                                              v_org, kv0, kv1, pb, hb, row);
             }
             if (nxt) {
                 if (narrow) {
@@ -1037,6 +1058,18 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// Opt-in dynamic shared memory per CTA of the current device.
+int max_dyn_smem()
+{
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 48 * 1024;
+    }
+    return v;
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode()
 {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1075,36 +1108,30 @@ ifdk_status launch_t(const BPParams& p, const CUtensorMap& map, const PTable& pt
 bool use_pair(const ifdk_geometry* g)
 {
     const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
-    const char* pe = std::getenv("IFDK_BP_PAIR");
-    return dv_max < 0.999 && !(pe && pe[0] == '0');
+    return dv_max < 0.999;
 }
 
-// Slices per floor of the k-walk when dv/dk < 1 for every z (all five configs): the PAIR
-// walk.  Default (5): issued on packed fp32x2 instructions with the taps read straight from
-// the TMA box (bp_raw_kernel; partial chunks at slab ends take walk 4) -- measured on B200
-// (config 4 / 3, 256 views, same session): 1880 / 1879 GUPS vs 1780 / 1784 for walk 4 (x2
-// walk on the rewritten pair patch) and ~1800 for the scalar walk 2.  All three are bitwise
-// equal.  IFDK_BP_WALK=2|3|4|5 overrides: 3 selects the TRIPLE walk where 0.5 <= dv/dk < 1
-// (configs 1-4), which needs 11 % less shared-memory traffic per update but measured slower
-// (1672 GUPS vs 1800 for scalar PAIR).  Otherwise 1 (IFDK_BP_PAIR=0 forces one floor per
-// slice, with 32-slice chunks).
-constexpr int kDefaultPairWalk = 5;
+// Tuning hook (ifdk_set_bp_variant): every walk it can select is bitwise equal to the
+// automatic choice, and the raster only reorders CTAs, so neither changes a result.
+std::atomic<int> g_walk_override{0}, g_raster_override{0};
 
+// Slices per floor of the k-walk.  Default where dv/dk < 1 for every z (all five configs):
+// the TRIPLE RAW walks -- 4-row (6) where 0.5 <= dv/dk (configs 1-4: 2000 vs 1884 GUPS for
+// the PAIR RAW walk on config 4), 3-row (7) where dv/dk < 0.5 everywhere (config 5) -- and
+// the PAIR RAW walk (5) in between; their partial chunks run on the pair-patch companions
+// 3, 8 and 4, bitwise equal.  dv/dk >= 1 somewhere: one floor per slice (walk 1, 32-slice
+// chunks).  The override (ifdk_set_bp_variant) picks among the bitwise-equal walks of the
+// geometry's family: 2, 4, 5 (PAIR), 3, 6 (4-row TRIPLE), 7, 8 (3-row TRIPLE).
 int choose_walk(const ifdk_geometry* g)
 {
     if (!use_pair(g)) return 1;
     const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
-    // TRIPLE RAW walks: 4-row where 0.5 <= dv/dk (configs 1-4: 2000 vs 1884 GUPS on config 4),
-    // 3-row where dv/dk < 0.5 everywhere (config 5)
     const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
-    int w = dv_min >= 0.5001 ? 6 : dv_max < 0.4999 ? 7 : kDefaultPairWalk;
-    if (const char* e = std::getenv("IFDK_BP_WALK")) {
-        const int v = std::atoi(e);
-        if (v == 2 || v == 4 || v == 5) w = v;
-        if (v == 6 && dv_min >= 0.5001) w = 6;  // 4-row TRIPLE RAW walk (configs 1-4)
-        if ((v == 7 || v == 8) && dv_max < 0.4999) w = v;  // 3-row TRIPLE (RAW / pair patch)
-        if (v == 3 && dv_min >= 0.5001) w = 3;
-    }
+    int w = dv_min >= 0.5001 ? 6 : dv_max < 0.4999 ? 7 : 5;
+    const int v = g_walk_override.load(std::memory_order_relaxed);
+    if (v == 2 || v == 4 || v == 5) w = v;
+    if ((v == 3 || v == 6) && dv_min >= 0.5001) w = v;
+    if ((v == 7 || v == 8) && dv_max < 0.4999) w = v;
     return w;
 }
 
@@ -1112,15 +1139,7 @@ int choose_walk(const ifdk_geometry* g)
 // only, never on the slab, so every decomposition of a volume walks identical chunks.
 // Measured on B200 (config 4): PAIR with 64 slices (2 CTAs/SM, 128 registers) 1724 GUPS vs
 // 32 slices (3 CTAs/SM, 80 registers) 1586; without PAIR 32 slices win.
-int choose_kc(const ifdk_geometry* g)
-{
-    const bool pair = use_pair(g);
-    if (const char* e = std::getenv("IFDK_BP_KC")) {
-        const int v = std::atoi(e);
-        if (v == 32 || (v == 64 && pair)) return v;
-    }
-    return pair ? 64 : 32;
-}
+int choose_kc(const ifdk_geometry* g) { return use_pair(g) ? 64 : 32; }
 
 }  // namespace
 
@@ -1160,12 +1179,10 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     // Raster band of 16 tile columns: measured on B200 (config 4, one 256-view launch) DRAM
     // traffic 49 GB (algorithmic 39 GB) and L2 hit rate 95 %, vs 354 GB and 65 % for the
     // row-major raster, at the same speed (the kernel is shared-memory bound).
-    // IFDK_BP_RASTER=n overrides (0 = row-major).
+    // ifdk_set_bp_variant(.., n) overrides (n >= tiles_i: row-major).
     p.raster = std::min(kRasterTiles, p.tiles_i);
-    if (const char* e = std::getenv("IFDK_BP_RASTER")) {
-        const int r = std::atoi(e);
+    if (const int r = g_raster_override.load(std::memory_order_relaxed))
         p.raster = (r > 0 && r < p.tiles_i) ? r : p.tiles_i;
-    }
     const bool tma_ok = box_h <= 256 && (g->Nu % 4) == 0 &&
                         (reinterpret_cast<uintptr_t>(Q) % 16) == 0 && get_encode() != nullptr;
 
@@ -1203,6 +1220,8 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS) tma = false;
+            // a box too large for the opt-in shared memory takes the global-memory walk
+            if (smem > (size_t)max_dyn_smem()) tma = false;
         }
         if (!tma) {
             P2 = 24;
@@ -1290,6 +1309,12 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
 }
 
 }  // namespace
+
+void set_bp_variant(int walk, int raster)
+{
+    g_walk_override.store(walk, std::memory_order_relaxed);
+    g_raster_override.store(raster, std::memory_order_relaxed);
+}
 
 ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,

@@ -37,7 +37,28 @@ struct FilterParams {
     int n_dest;
     float* base[kMaxFilterDest];
     int lo[kMaxFilterDest], hi[kMaxFilterDest];
+    // Completion signal of the fused exchange (flags.n > 0; peer.cu): after its stores every
+    // thread fences at system scope, and the CTA that takes the last ticket increments the
+    // flags -- the destinations' consumers wait on them.
+    PeerFlags flags;
 };
+
+// The "last block" pattern at system scope (CUDA C++ Programming Guide, Memory Fence
+// Functions): every row this launch stored is visible to the peers before any flag moves.
+__device__ __forceinline__ void signal_done(const FilterParams& p)
+{
+    if (p.flags.n == 0) return;
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned ticket = atomicAdd(p.flags.ticket, 1u);
+        if (ticket == gridDim.x - 1) {
+            __threadfence_system();
+            for (int f = 0; f < p.flags.n; ++f) atomicAdd_system(p.flags.flag[f], 1u);
+            atomicExch(p.flags.ticket, 0u);  // ready for the next launch on the stream
+        }
+    }
+}
 
 // Output row r (= t n_rows + (v - v0)) of destination d, or nullptr if v is outside its band.
 __device__ __forceinline__ float* dest_row(const FilterParams& p, long r, int d)
@@ -170,6 +191,7 @@ __global__ void __launch_bounds__(kThreads) filter_fft_kernel(const FilterParams
         }
         __syncthreads();
     }
+    signal_done(p);
 }
 
 
@@ -476,12 +498,14 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
         }
     }
     if (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
+    signal_done(p);
 }
 
 }  // namespace
 
 ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
-                          int n_rows, cudaStream_t st, int n_dest, const ifdk_band_dest* dests)
+                          int n_rows, cudaStream_t st, int n_dest, const ifdk_band_dest* dests,
+                          const PeerFlags* flags)
 {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -521,7 +545,7 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
         }
     }
     const long total = n_views * (long)n_rows;
-    if (total == 0) return IFDK_OK;
+    if (total == 0) return flags ? launch_signal(*flags, st) : IFDK_OK;
     const int L = 1 << g->log2L;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -544,6 +568,7 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
         p.lo[d] = d < n_dest ? dests[d].v_lo : 0;
         p.hi[d] = d < n_dest ? dests[d].v_hi : -1;
     }
+    if (flags) p.flags = *flags;
     const long pairs = (total + 1) / 2;
     if (L == 4096) {
         // row pairs per transform: the largest R <= 8 whose slot 4096 / R holds a full-length

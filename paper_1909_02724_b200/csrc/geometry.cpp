@@ -137,8 +137,8 @@ extern "C" ifdk_status ifdk_geometry_create(int Nu, int Nv, int Nx, int Ny, int 
             return fail(IFDK_ERR_INVALID_ARGUMENT, "every pitch must be finite and > 0");
     if (!(d > 0.0) || !(D > d) || !std::isfinite(D))
         return fail(IFDK_ERR_INVALID_ARGUMENT, "need 0 < d < D (finite)");
-    if (!std::isfinite(theta) || theta == 0.0)
-        return fail(IFDK_ERR_INVALID_ARGUMENT, "theta must be finite and non-zero");
+    if (!std::isfinite(theta) || !(theta > 0.0))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "theta must be finite and > 0");
     auto* g = new ifdk_geometry();
     g->Nu = Nu; g->Nv = Nv; g->Nx = Nx; g->Ny = Ny; g->Nz = Nz;
     g->Du = Du; g->Dv = Dv; g->Dx = Dx; g->Dy = Dy; g->Dz = Dz;

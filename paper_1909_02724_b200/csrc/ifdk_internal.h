@@ -55,14 +55,28 @@ void patch_bound(const ifdk_geometry* g, int ti, int tj, int kc, double* w, doub
 
 // filter.cu (n_dest > 0: write each row to the destination bands instead of `out`)
 constexpr int kMaxFilterDest = 16;
+
+// Device words incremented (system-scope atomics) once a launch's stores are complete
+// (peer.cu): the signals of the fused exchange.
+struct PeerFlags {
+    int n = 0;
+    unsigned int* flag[kMaxFilterDest] = {};
+    unsigned int* ticket = nullptr;  // device word, 0 between launches ("last CTA" counter)
+};
+
 ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
                           int n_rows, cudaStream_t st, int n_dest = 0,
-                          const ifdk_band_dest* dests = nullptr);
+                          const ifdk_band_dest* dests = nullptr, const PeerFlags* flags = nullptr);
+
+// peer.cu: flags[i] += 1 after all earlier work on the stream
+ifdk_status launch_signal(const PeerFlags& f, cudaStream_t st);
 
 // backproject.cu
 ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
                                cudaStream_t st);
+// tuning hook behind ifdk_set_bp_variant (0 = automatic)
+void set_bp_variant(int walk, int raster);
 
 // forward.cu: the matched forward projector (transpose of launch_backproject) and the
 // element-wise SART / SIRT steps

@@ -20,6 +20,12 @@ Two decompositions of the paper's R x C rank grid on one node:
   k-slabs replaces the paper's single MPI_Reduce.  Needs a full
   volume per GPU, so it does not fit config 5.
 
+The band exchange is fused into the filter by default: ``PeerExchange`` maps every rank's
+receive buffer into every other rank (CUDA IPC over NVLink), ``ifdk_filter_scatter`` stores
+each filtered row straight into the destination bands, and device-side signals
+(``ifdk_signal`` / ``ifdk_wait``) order the stores before the peers' back-projection and
+the buffer reuse after it.  NCCL ``all_to_all_single`` is the baseline (``exchange="nccl"``).
+
 ``kslab_reconstruct_host`` is the end-to-end form: raw blocks come from pinned host
 memory (H2D on a copy stream, one round ahead) and the finished slab goes back to the
 host in sub-slabs while the last round's back-projection continues.
@@ -218,50 +224,166 @@ def _default_fns(g, filter_fn, bp_fn):
     return filter_fn, bp_fn
 
 
+class PeerExchange:
+    """Receive buffers of the fused row-band exchange, one per rank and mapped into every rank
+    (CUDA IPC: NVLink peer memory between GPUs), plus the signal words that order the peers'
+    stores (ifdk_filter_scatter's completion flags, ifdk_signal / ifdk_wait; the ordering
+    argument is in csrc/peer.cu).
+
+    Layout of rank h's buffer (bytes): [0, 256) uint32 landed[r] = rounds of rank r's rows
+    that have landed in h's receive area; [256, 512) uint32 freed[r] = rounds rank r has
+    back-projected (buffer releases); [512, 516) the ticket of h's own scatter launches;
+    [1024, ...) the fp32 receive area, two rounds deep: 2 * recv_max[h] floats.  Every rank
+    signals every other rank once per round (rows or not), so after round t every landed[r]
+    is t + 1 and, once its back-projection is done, every freed[r] is t + 1.
+
+    ``create`` builds one over a process group (IPC handles exchanged with all_gather_object);
+    ``local`` builds all ranks' exchanges in one process on one GPU (virtual ranks, tests)."""
+
+    HEADER = 1024
+
+    def __init__(self, rank, world, bases, recv_max, own=(), opened=()):
+        if world > 16:
+            raise ValueError("the fused exchange signals at most 16 ranks")
+        self.rank, self.world = rank, world
+        self.bases = [int(b) for b in bases]
+        self.recv_max = list(recv_max)
+        self._own, self._opened = list(own), list(opened)
+        self.kind = "p2p-fused"
+
+    # -- construction
+    @staticmethod
+    def _alloc(recv_max):
+        from .ifdk import as_tensor, peer_alloc
+
+        ptr, handle = peer_alloc(PeerExchange.HEADER + 8 * max(int(recv_max), 1))
+        as_tensor(ptr, (PeerExchange.HEADER // 4,), "uint32").zero_()
+        return ptr, handle
+
+    @classmethod
+    def create(cls, group, rank, world, recv_max):
+        import torch
+        import torch.distributed as dist
+
+        from .ifdk import peer_open
+
+        ptr, handle = cls._alloc(recv_max[rank])
+        handles = [None] * world
+        dist.all_gather_object(handles, handle, group=group)
+        bases, opened = [], []
+        for h in range(world):
+            if h == rank:
+                bases.append(ptr)
+            else:
+                q = peer_open(handles[h])
+                bases.append(q)
+                opened.append(q)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every header zeroed before anyone signals
+        return cls(rank, world, bases, recv_max, own=[ptr], opened=opened)
+
+    @classmethod
+    def local(cls, world, recv_max):
+        ptrs = [cls._alloc(recv_max[h])[0] for h in range(world)]
+        ex = [cls(r, world, ptrs, recv_max) for r in range(world)]
+        ex[0]._own = ptrs  # rank 0's object frees them all
+        return ex
+
+    def close(self):
+        from .ifdk import peer_close, peer_free
+
+        for q in self._opened:
+            peer_close(q)
+        for q in self._own:
+            peer_free(q)
+        self._opened, self._own = [], []
+
+    # -- addressing
+    def _area(self, h, q, off):
+        return self.bases[h] + self.HEADER + 4 * (q * self.recv_max[h] + off)
+
+    def recv(self, q, off, rn, rows, Nu):
+        """My receive area q at element offset off as a [rn][rows][Nu] tensor."""
+        from .ifdk import as_tensor
+
+        return as_tensor(self._area(self.rank, q, off), (rn, rows, Nu))
+
+    def _landed_flags(self):
+        return [b + 4 * self.rank for b in self.bases]
+
+    # -- the round protocol (each call enqueues on the current stream)
+    def wait_free(self, t):
+        """Before scattering round t: every rank has released buffer t % 2 (round t - 2)."""
+        from .ifdk import ifdk_wait
+
+        if t >= 2:
+            ifdk_wait(self.bases[self.rank] + 256, self.world, t - 1)
+
+    def scatter(self, g, src, q, bands, filter_fn=None):
+        """Filter src (the rank's block of this round, None if it has none) into every
+        destination band: bands = [(h, off, lo, hi)] (element offset off in h's receive
+        layout); raises every rank's landed word once all rows have been stored.  The filter
+        is ifdk_filter_scatter's (bitwise ifdk_filter's); filter_fn is for host fakes."""
+        from .ifdk import ifdk_filter_scatter, ifdk_signal
+
+        dests = [(self._area(h, q, off), lo, hi) for h, off, lo, hi in bands]
+        if src is not None and dests:
+            ifdk_filter_scatter(g, src, dests, flags=self._landed_flags(),
+                                ticket=self.bases[self.rank] + 512)
+        else:
+            ifdk_signal(self._landed_flags())
+
+    def wait_landed(self, t):
+        from .ifdk import ifdk_wait
+
+        ifdk_wait(self.bases[self.rank], self.world, t + 1)
+
+    def release(self):
+        """After back-projecting a round: tell every rank its buffer here may be reused."""
+        from .ifdk import ifdk_signal
+
+        ifdk_signal([b + 256 + 4 * self.rank for b in self.bases])
+
+
 _P2P_CACHE: dict = {}
 
 
-def _p2p_buffers(group, numel, dev):
-    """A float32 symmetric-memory buffer of `numel` elements on every rank of `group` and its
-    handle (peer pointers over NVLink, device-side barrier), or None if unavailable.  Cached:
-    the rendezvous is a collective and the allocation persists across calls."""
+def _peer_exchange(group, rank, world, recv_max, dev):
+    """A PeerExchange over `group` (cached: creation is collective and the buffers persist),
+    or None on every rank if any rank cannot map its peers."""
     import torch
     import torch.distributed as dist
 
-    pg = group or dist.group.WORLD
-    key = (id(pg), numel, str(dev))
+    key = (id(group or dist.group.WORLD), rank, world, tuple(recv_max), str(dev))
     if key in _P2P_CACHE:
         return _P2P_CACHE[key]
-    hdl, buf = None, None
+    ex, err = None, None
     try:
-        import torch.distributed._symmetric_memory as symm_mem
-
-        buf = symm_mem.empty(numel, dtype=torch.float32, device=dev)
-        hdl = symm_mem.rendezvous(buf, pg)
-    except Exception as exc:  # noqa: BLE001 -- no P2P/symmetric memory: the NCCL exchange
+        ex = PeerExchange.create(group, rank, world, recv_max)
+    except Exception as exc:  # noqa: BLE001 -- no peer mapping: the NCCL band exchange
+        err = exc
+    ok = torch.tensor([1 if ex is not None else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if int(ok.item()) == 0:
         import warnings
 
-        warnings.warn(f"symmetric memory unavailable, NCCL band exchange: {exc!r}")
-        hdl = None
-    # every rank must take the same path
-    ok = torch.tensor([1 if hdl is not None else 0], device=dev)
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=pg)
-    if int(ok.item()) == 0:
-        hdl = None
-    _P2P_CACHE[key] = hdl
-    _P2P_CACHE[key + ("buffer",)] = buf  # the handle does not own the allocation
-    return hdl
-
-
-def _ifdk_scatter(g, raw, dests):
-    from .ifdk import ifdk_filter_scatter
-
-    ifdk_filter_scatter(g, raw, dests)
+        warnings.warn(f"peer memory unavailable, NCCL band exchange: {err!r}")
+        if ex is not None:
+            ex.close()
+        ex = None
+    if ex is not None:
+        if len(_P2P_CACHE) > 4:
+            for old in _P2P_CACHE.values():
+                if old is not None:
+                    old.close()
+            _P2P_CACHE.clear()
+        _P2P_CACHE[key] = ex
+    return ex
 
 
 def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, timings,
               raw_local=None, raw_host=None, vol_host=None, force_exchange=False,
-              exchange="auto", scatter_fn=None):
+              exchange="auto", peer=None):
     import torch
     import torch.distributed as dist
 
@@ -283,26 +405,27 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
         offs.append(o)
         o += n
     B = plan.block
-    # Persistent double buffers (no allocator traffic across streams).
-    Qbuf = [torch.empty((B, Nv, Nu), device=dev) for _ in range(min(2, rounds))]
     send_max = max([sum(e.send_sizes) for e in exs] + [1])
-    recv_max = max([sum(e.recv_sizes) for e in exs] + [1])
-    p2p = _p2p_buffers(group, 2 * recv_max, dev) if (xchg and cuda and exchange != "nccl") \
-        else None
-    if p2p is not None:
-        sym = p2p.get_buffer(p2p.rank, (2 * recv_max,), torch.float32)
-        recvbuf = [sym[:recv_max], sym[recv_max:]]
-        sendbuf = None
+    # receive-area size of every rank (the fused exchange addresses the destination's layout)
+    recv_max_all = [max([sum(e.recv_sizes) for e in exchanges(g, plan, h)] + [1])
+                    for h in range(world)]
+    recv_max = recv_max_all[rank]
+    if peer is None and xchg and cuda and exchange in ("auto", "p2p"):
+        peer = _peer_exchange(group, rank, world, recv_max_all, dev)
+        if peer is None and exchange == "p2p":
+            raise RuntimeError("exchange='p2p': peer memory unavailable")
+    if not xchg:
+        peer = None
+    nbuf = min(2, rounds)
+    if peer is not None:
+        Qbuf = [None] * nbuf
+        sendbuf = recvbuf = None
         # element offset of my band inside destination h's receive layout, per round
-        p2p_off = []
-        for t in range(rounds):
-            offs_t = []
-            for h in range(world):
-                exh = exchanges(g, plan, h)[t]
-                offs_t.append(sum(exh.recv_sizes[:rank]))
-            p2p_off.append(offs_t)
-        scatter_fn = scatter_fn or (lambda raw, dests: _ifdk_scatter(g, raw, dests))
+        p2p_off = [[sum(exchanges(g, plan, h)[t].recv_sizes[:rank]) for h in range(world)]
+                   for t in range(rounds)]
     else:
+        # Persistent double buffers (no allocator traffic across streams).
+        Qbuf = [torch.empty((B, Nv, Nu), device=dev) for _ in range(nbuf)]
         sendbuf = [torch.empty(send_max, device=dev) for _ in Qbuf] if xchg else None
         recvbuf = [torch.empty(recv_max, device=dev) for _ in Qbuf] if xchg else None
     stage = [torch.empty((B, Nv, Nu), device=dev) for _ in Qbuf] if raw_host is not None else None
@@ -353,18 +476,17 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
                 else:
                     src = raw_local[offs[bi]:offs[bi] + n]
             work = None
-            if xchg and p2p is not None:
-                # fused: every filtered row goes straight into the receive buffers of the
-                # slabs that need it (NVLink stores into peer memory); the first barrier
-                # guarantees every rank's BP of round t-2 has released buffer q, the second
-                # that every rank's rows have landed (system-scope release / acquire).
-                p2p.barrier(channel=0)
+            if peer is not None:
+                # fused: every filtered row goes straight into the receive areas of the slabs
+                # that need it (NVLink stores into peer memory).  Before: every rank has
+                # released area q (its BP of round t - 2 is done); after the last store the
+                # kernel raises this rank's landed word on every rank (csrc/peer.cu).
+                peer.wait_free(t)
+                bands = [(h, p2p_off[t][h], lo, hi) for h, (lo, hi) in enumerate(ex.send)
+                         if hi >= lo]
+                peer.scatter(g, src if n > 0 else None, q, bands, filter_fn)
                 if n > 0:
-                    dests = [(p2p.buffer_ptrs[h] + 4 * (q * recv_max + p2p_off[t][h]), lo, hi)
-                             for h, (lo, hi) in enumerate(ex.send) if hi >= lo]
-                    scatter_fn(src, dests)
                     bi += 1
-                p2p.barrier(channel=0)
                 e1 = S.event(True)
                 S.record(e1, S.F)
                 f_marks.append((e0, e1))
@@ -400,6 +522,8 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
             if work is not None:
                 work.wait()  # the BP stream waits for the collective
             S.wait(S.B, ev_ready)
+            if peer is not None:
+                peer.wait_landed(t)  # every rank's round-t rows are in my area q
             b0 = S.event(True)
             S.record(b0, S.B)
             last = t == rounds - 1
@@ -416,7 +540,9 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
                     lo, hi = ex.recv[r]
                     sz = ex.recv_sizes[r]
                     if rn > 0 and sz > 0 and nk > 0:
-                        if xchg:
+                        if peer is not None:
+                            band, v0 = peer.recv(q, off, rn, hi - lo + 1, Nu), lo
+                        elif xchg:
                             band, v0 = recvbuf[q][off:off + sz].view(rn, hi - lo + 1, Nu), lo
                         else:  # one rank: back-project straight from the filtered block
                             band, v0 = Qbuf[q][:rn], 0
@@ -438,6 +564,8 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
                         c1 = S.event(True)
                         S.record(c1, S.C)
                         c_marks.append((c0, c1))
+            if peer is not None:
+                peer.release()  # my area q may be refilled (round t + 2)
             if launched:
                 first_bp = False
             b1 = S.event(True)
@@ -462,8 +590,9 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
         tc = sum(a.elapsed_time(b) for a, b in c_marks)
         timings.update({"wall_ms": wall, "filter_pack_ms": tf, "bp_ms": tb, "host_copy_ms": tc,
                         "rounds": rounds,
-                        "exchange": ("p2p-fused" if p2p is not None else "nccl") if xchg
+                        "exchange": (peer.kind if peer is not None else "nccl") if xchg
                         else "none",
+                        "delta": (tf + tb + tc) / wall if wall > 0 else None,
                         "exchange_bytes_sent": 4 * sum(sum(e.send_sizes) - e.send_sizes[rank]
                                                        for e in exs) if xchg else 0})
     return vol_slab
@@ -472,27 +601,30 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
 def kslab_reconstruct(g, raw_local, vol_slab, plan: SlabPlan, rank: int, group=None,
                       filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
                       timings: Optional[dict] = None, force_exchange: bool = False,
-                      exchange: str = "auto"):
+                      exchange: str = "auto", peer: Optional[PeerExchange] = None):
     """k-slab FDK on one rank.  raw_local: [plan.n_local(rank)][Nv][Nu], the rank's blocks
     (plan.local_views(rank)) in order, device-resident; vol_slab: [nk][Ny][Nx] (slab
     plan.slab(rank)), overwritten.  Enqueued on side streams that the current stream joins.
-    exchange: "auto" fuses the band exchange into the filter over symmetric (NVLink peer)
-    memory when the group supports it (ifdk_filter_scatter + device barriers), else NCCL
-    all-to-all; "nccl" forces the all-to-all."""
+    exchange: "auto" fuses the band exchange into the filter over peer (NVLink) memory when
+    every rank can map its peers (PeerExchange: ifdk_filter_scatter + device-side signals),
+    else NCCL all-to-all; "p2p" requires the fused exchange; "nccl" forces the all-to-all.
+    peer: an existing PeerExchange (e.g. PeerExchange.local for virtual ranks on one GPU)."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
-                     raw_local=raw_local, force_exchange=force_exchange, exchange=exchange)
+                     raw_local=raw_local, force_exchange=force_exchange, exchange=exchange,
+                     peer=peer)
 
 
 def kslab_reconstruct_host(g, raw_host, vol_slab, vol_host, plan: SlabPlan, rank: int,
                            group=None, filter_fn: Optional[Callable] = None,
                            bp_fn: Optional[Callable] = None, timings: Optional[dict] = None,
-                           force_exchange: bool = False, exchange: str = "auto"):
+                           force_exchange: bool = False, exchange: str = "auto",
+                           peer: Optional[PeerExchange] = None):
     """End-to-end k-slab FDK on one rank: raw_host (pinned, the rank's blocks in order) is
     copied block by block one round ahead; vol_slab (device scratch [nk][Ny][Nx]) is
     streamed to vol_host (pinned) in sub-slabs during the last round."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
                      raw_host=raw_host, vol_host=vol_host, force_exchange=force_exchange,
-                     exchange=exchange)
+                     exchange=exchange, peer=peer)
 
 
 # ----------------------------------------------------------------------------- R x C grid
@@ -541,7 +673,8 @@ def grid_groups(grid: GridPlan):
 
 def hybrid_reconstruct(g, raw_local, vol_sub, grid: GridPlan, rank: int, row_group, col_group,
                        filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
-                       timings: Optional[dict] = None, exchange: str = "auto"):
+                       timings: Optional[dict] = None, exchange: str = "auto",
+                       peer: Optional[PeerExchange] = None):
     """R x C FDK on one rank.  raw_local: the rank's blocks of its column
     (grid.column_plan(c).local_views(r)) in order; vol_sub: [n][Ny][Nx] for
     grid.sub_slab(rank), overwritten.  Equal to one GPU up to fp32 summation order (the C
@@ -556,7 +689,7 @@ def hybrid_reconstruct(g, raw_local, vol_sub, grid: GridPlan, rank: int, row_gro
     partial = raw_local.new_empty((q * grid.C, g.Ny, g.Nx))
     partial[nk:].zero_()  # padding rows of the reduce-scatter
     _pipeline(g, plan, r, partial[:nk], col_group, filter_fn, bp_fn, timings,
-              raw_local=raw_local, exchange=exchange)
+              raw_local=raw_local, exchange=exchange, peer=peer)
     sk0, sn = grid.sub_slab(rank)
     if grid.C > 1:
         out = raw_local.new_empty((q, g.Ny, g.Nx))

@@ -14,8 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# IFDK_LIB may point at another build of the same library (A/B timing of kernel variants).
-LIB_PATH = os.environ.get("IFDK_LIB") or os.path.join(_HERE, "libifdk.so")
+LIB_PATH = os.path.join(_HERE, "libifdk.so")
 
 IFDK_OK = 0
 STATUS_NAMES = {
@@ -35,6 +34,12 @@ EXPORTS = (
     "ifdk_band_rows",
     "ifdk_filter",
     "ifdk_filter_scatter",
+    "ifdk_peer_alloc",
+    "ifdk_peer_open",
+    "ifdk_peer_close",
+    "ifdk_peer_free",
+    "ifdk_signal",
+    "ifdk_wait",
     "ifdk_backproject",
     "ifdk_backproject_alg2",
     "ifdk_backproject_alg4",
@@ -47,6 +52,7 @@ EXPORTS = (
     "ifdk_mlem_ratio",
     "ifdk_mlem_update",
     "ifdk_fill",
+    "ifdk_set_bp_variant",
     "ifdk_last_launch_count",
     "ifdk_last_error",
 )
@@ -79,8 +85,21 @@ class _BandDest(ctypes.Structure):
     _fields_ = [("base", ctypes.c_void_p), ("v_lo", ctypes.c_int), ("v_hi", ctypes.c_int)]
 
 
-_lib.ifdk_filter_scatter.argtypes = [_vp, _vp, _l, _i, _i, _i, ctypes.POINTER(_BandDest), _vp]
+_lib.ifdk_filter_scatter.argtypes = [_vp, _vp, _l, _i, _i, _i, ctypes.POINTER(_BandDest), _i,
+                                     ctypes.POINTER(_vp), _vp, _vp]
 _lib.ifdk_filter_scatter.restype = _i
+_lib.ifdk_peer_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp), ctypes.c_char_p]
+_lib.ifdk_peer_alloc.restype = _i
+_lib.ifdk_peer_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(_vp)]
+_lib.ifdk_peer_open.restype = _i
+_lib.ifdk_peer_close.argtypes = [_vp]
+_lib.ifdk_peer_close.restype = _i
+_lib.ifdk_peer_free.argtypes = [_vp]
+_lib.ifdk_peer_free.restype = _i
+_lib.ifdk_signal.argtypes = [_i, ctypes.POINTER(_vp), _vp]
+_lib.ifdk_signal.restype = _i
+_lib.ifdk_wait.argtypes = [_vp, _i, ctypes.c_uint, _vp]
+_lib.ifdk_wait.restype = _i
 _lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp]
 _lib.ifdk_backproject.restype = _i
 _lib.ifdk_backproject_alg2.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _i, _i, _vp]
@@ -105,6 +124,8 @@ _lib.ifdk_mlem_update.argtypes = [_vp, _vp, _vp, _l, _vp]
 _lib.ifdk_mlem_update.restype = _i
 _lib.ifdk_fill.argtypes = [_vp, ctypes.c_float, _l, _vp]
 _lib.ifdk_fill.restype = _i
+_lib.ifdk_set_bp_variant.argtypes = [_i, _i]
+_lib.ifdk_set_bp_variant.restype = _i
 _lib.ifdk_last_launch_count.argtypes = []
 _lib.ifdk_last_launch_count.restype = _i
 _lib.ifdk_last_error.argtypes = []
@@ -114,6 +135,12 @@ _lib.ifdk_last_error.restype = ctypes.c_char_p
 def _check(st: int) -> None:
     if st != IFDK_OK:
         raise IfdkError(st, _lib.ifdk_last_error().decode())
+
+
+def set_bp_variant(walk: int = 0, raster: int = 0) -> None:
+    """Speed-tuning hook (A/B runs, tests): pick a back-projection walk among the variants
+    that are bitwise equal to the automatic one, and the CTA raster band; 0 = automatic."""
+    _check(_lib.ifdk_set_bp_variant(int(walk), int(raster)))
 
 
 def last_launch_count() -> int:
@@ -191,16 +218,74 @@ def ifdk_filter(g: Geometry, raw, filtered, v0: int = 0, stream=None) -> None:
                             raw.shape[0], int(v0), raw.shape[1], _stream_ptr(stream)))
 
 
-def ifdk_filter_scatter(g: Geometry, raw, dests, v0: int = 0, stream=None) -> None:
+def _ptr_array(ptrs):
+    return (_vp * max(len(ptrs), 1))(*[int(x) for x in ptrs])
+
+
+def ifdk_filter_scatter(g: Geometry, raw, dests, v0: int = 0, flags=(), ticket: int = 0,
+                        stream=None) -> None:
     """Alg. alg:filter of raw [n_views][n_rows][Nu] (rows v0..), each filtered row stored into
     every destination band that holds it.  dests: list of (ptr, v_lo, v_hi) where ptr is a
-    device pointer (int, e.g. tensor.data_ptr() or a peer-mapped symmetric-memory address) to
-    an [n_views][v_hi - v_lo + 1][Nu] fp32 buffer."""
+    device pointer (int: tensor.data_ptr() or a peer-mapped ifdk_peer_open address) to an
+    [n_views][v_hi - v_lo + 1][Nu] fp32 buffer.  flags: device pointers of uint32 words, each
+    incremented once all rows have landed (system scope); ticket: a device uint32 word that is
+    0 (required with flags)."""
     if raw.dim() != 3 or raw.shape[2] != g.Nu:
         raise ValueError("raw must be [n_views][n_rows][Nu]")
     arr = (_BandDest * len(dests))(*[_BandDest(int(b), int(lo), int(hi)) for b, lo, hi in dests])
     _check(_lib.ifdk_filter_scatter(g.handle, _dev_f32(raw, "raw"), raw.shape[0], int(v0),
-                                    raw.shape[1], len(dests), arr, _stream_ptr(stream)))
+                                    raw.shape[1], len(dests), arr, len(flags), _ptr_array(flags),
+                                    int(ticket) or None, _stream_ptr(stream)))
+
+
+def peer_alloc(nbytes: int) -> tuple[int, bytes]:
+    """ifdk_peer_alloc: (device pointer, 64-byte IPC handle) of a fresh cudaMalloc."""
+    ptr = _vp()
+    h = ctypes.create_string_buffer(64)
+    _check(_lib.ifdk_peer_alloc(int(nbytes), ctypes.byref(ptr), h))
+    return int(ptr.value), bytes(h.raw)
+
+
+def peer_open(handle: bytes) -> int:
+    """ifdk_peer_open: map another process's peer buffer; returns its device pointer here."""
+    ptr = _vp()
+    _check(_lib.ifdk_peer_open(bytes(handle), ctypes.byref(ptr)))
+    return int(ptr.value)
+
+
+def peer_close(ptr: int) -> None:
+    _check(_lib.ifdk_peer_close(int(ptr) or None))
+
+
+def peer_free(ptr: int) -> None:
+    _check(_lib.ifdk_peer_free(int(ptr) or None))
+
+
+def ifdk_signal(flags, stream=None) -> None:
+    """After earlier work on the stream, each device uint32 word in `flags` += 1 (system scope)."""
+    _check(_lib.ifdk_signal(len(flags), _ptr_array(flags), _stream_ptr(stream)))
+
+
+def ifdk_wait(flags_ptr: int, n: int, target: int, stream=None) -> None:
+    """Later work on the stream waits until the n uint32 words at flags_ptr reach target."""
+    _check(_lib.ifdk_wait(int(flags_ptr), int(n), int(target) & 0xFFFFFFFF, _stream_ptr(stream)))
+
+
+class DeviceArray:
+    """A CUDA array view of raw device memory (e.g. a peer buffer) for torch.as_tensor:
+    __cuda_array_interface__ with the caller keeping the memory alive."""
+
+    def __init__(self, ptr: int, shape, typestr: str = "<f4"):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape),
+                                         "typestr": typestr, "version": 3, "strides": None}
+
+
+def as_tensor(ptr: int, shape, dtype: str = "float32"):
+    """torch tensor over device memory at ptr (no copy; memory owned elsewhere)."""
+    import torch
+
+    ts = {"float32": "<f4", "uint32": "<u4", "int32": "<i4"}[dtype]
+    return torch.as_tensor(DeviceArray(ptr, shape, ts), device="cuda")
 
 
 def ifdk_backproject(g: Geometry, filtered, s0: int, vol, k0: int = 0, v0: int = 0,

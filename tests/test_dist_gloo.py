@@ -1,5 +1,6 @@
-"""Multi-rank host logic of the k-slab and projection-split drivers, world size 2 and 3
-over gloo on CPU.  The compute is injected (fp64 oracle filter / back-projection), so
+"""Multi-rank host logic of the k-slab and projection-split drivers, world size 2 to 4
+over gloo on CPU (the fused exchange's round protocol through a shared-memory fake of
+dist.PeerExchange).  The compute is injected (fp64 oracle filter / back-projection), so
 these tests check the plan, the row-band all-to-all and the reduce-scatter bookkeeping;
 the oracle raises if any rank is missing a detector row its slab taps."""
 import os
@@ -52,6 +53,81 @@ def _reference():
     return E, oracle.backproject_volume(og, Q32.astype(np.float64))
 
 
+class HostPeerExchange:
+    """Host fake of dist.PeerExchange for the gloo tests: the same round protocol (wait_free,
+    scatter, wait_landed, release) and buffer layout, with POSIX shared memory standing in for
+    the NVLink-mapped receive buffers and host spin-waits for ifdk_wait.  Each signal word has
+    a single writer (rank r writes landed[r] / freed[r] in every buffer), as on the GPU."""
+
+    kind = "host-fake"
+
+    def __init__(self, tag, rank, world, recv_max):
+        import time
+        from multiprocessing import shared_memory
+
+        import torch.distributed as dist
+
+        self.rank, self.world, self.recv_max = rank, world, list(recv_max)
+        self._time = time
+        hdr = 2 * world * 8
+        self.shm = [None] * world
+        self.shm[rank] = shared_memory.SharedMemory(
+            name=f"{tag}_{rank}", create=True, size=hdr + 8 * max(recv_max[rank], 1))
+        self.shm[rank].buf[:hdr] = bytes(hdr)
+        dist.barrier()
+        for h in range(world):
+            if h != rank:
+                self.shm[h] = shared_memory.SharedMemory(name=f"{tag}_{h}")
+        self.words = [np.ndarray((2, world), np.int64, buffer=m.buf) for m in self.shm]
+        self.area = [np.ndarray((2 * max(recv_max[h], 1),), np.float32, buffer=m.buf, offset=hdr)
+                     for h, m in enumerate(self.shm)]
+        dist.barrier()
+
+    def close(self):
+        import torch.distributed as dist
+
+        self.words = self.area = None
+        dist.barrier()
+        for h, m in enumerate(self.shm):
+            m.close()
+            if h == self.rank:
+                m.unlink()
+
+    def _wait(self, row, target):
+        t0 = self._time.time()
+        while (self.words[self.rank][row] < target).any():
+            if self._time.time() - t0 > 120:
+                raise TimeoutError(f"rank {self.rank}: signal row {row} never reached {target}")
+            self._time.sleep(0.0005)
+
+    def wait_free(self, t):
+        if t >= 2:
+            self._wait(1, t - 1)
+
+    def scatter(self, g, src, q, bands, filter_fn):
+        if src is not None and bands:
+            Q = torch.empty_like(src)
+            filter_fn(src, Q)
+            n = src.shape[0]
+            for h, off, lo, hi in bands:
+                a = q * self.recv_max[h] + off
+                dst = self.area[h][a:a + n * (hi - lo + 1) * g.Nu]
+                dst.reshape(n, hi - lo + 1, g.Nu)[:] = Q[:, lo:hi + 1, :].numpy()
+        for h in range(self.world):  # stores first, then the single-writer landed word
+            self.words[h][0, self.rank] += 1
+
+    def wait_landed(self, t):
+        self._wait(0, t + 1)
+
+    def recv(self, q, off, rn, rows, Nu):
+        a = q * self.recv_max[self.rank] + off
+        return torch.from_numpy(self.area[self.rank][a:a + rn * rows * Nu].reshape(rn, rows, Nu))
+
+    def release(self):
+        for h in range(self.world):
+            self.words[h][1, self.rank] += 1
+
+
 def _worker(rank, world, port, mode, out_q):
     import torch.distributed as dist
 
@@ -63,7 +139,7 @@ def _worker(rank, world, port, mode, out_q):
         g = Geometry.from_spec(SPEC)
         f, b = _oracle_fns(og)
         E, ref = _reference()
-        if mode in ("kslab", "kslab_host"):
+        if mode in ("kslab", "kslab_host", "kslab_fused"):
             # 8-view blocks: 5 blocks of 36 views, several pipelined rounds and a short last one
             plan = SlabPlan(world, SPEC.Nz, SPEC.Np, block=8)
             k0, nk = plan.slab(rank)
@@ -72,6 +148,17 @@ def _worker(rank, world, port, mode, out_q):
             vol = torch.empty((nk, SPEC.Ny, SPEC.Nx))
             if mode == "kslab":
                 kslab_reconstruct(g, torch.from_numpy(mine), vol, plan, rank, filter_fn=f, bp_fn=b)
+            elif mode == "kslab_fused":
+                # the fused exchange's round protocol (dist.PeerExchange) with the host fake
+                from paper_1909_02724_b200.dist import exchanges
+
+                rmax = [max(sum(e.recv_sizes) for e in exchanges(g, plan, h)) for h in range(world)]
+                peer = HostPeerExchange(f"ifdk_{port}", rank, world, rmax)
+                try:
+                    kslab_reconstruct(g, torch.from_numpy(mine), vol, plan, rank, filter_fn=f,
+                                      bp_fn=b, peer=peer)
+                finally:
+                    peer.close()
             else:
                 host = torch.full((nk, SPEC.Ny, SPEC.Nx), float("nan"))
                 kslab_reconstruct_host(g, torch.from_numpy(mine), vol, host, plan, rank,
@@ -105,6 +192,8 @@ def _worker(rank, world, port, mode, out_q):
 
 
 @pytest.mark.parametrize("world,mode", [(2, "kslab"), (3, "kslab"), (2, "kslab_host"),
+                                        (2, "kslab_fused"), (3, "kslab_fused"),
+                                        (4, "kslab_fused"),
                                         (2, "projsplit"), (4, "grid22"), (3, "grid13"),
                                         (3, "grid31")])
 def test_multi_rank_matches_single(world, mode):

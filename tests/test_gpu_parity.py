@@ -22,6 +22,15 @@ def torch_cuda():
     return torch
 
 
+@pytest.fixture
+def auto_variant():
+    """Restores the automatic BP walk after a test that pins one (ifdk_set_bp_variant)."""
+    yield
+    from paper_1909_02724_b200 import set_bp_variant
+
+    set_bp_variant(0, 0)
+
+
 def _spec(Np, Nu, Nv, Nx, Ny, Nz, **kw):
     return synth.ConfigSpec(f"{Np}x{Nu}x{Nv}->{Nx}x{Ny}x{Nz}", Np, Nu, Nv, Nx, Ny, Nz, **kw)
 
@@ -183,7 +192,7 @@ def test_bp_slab_split_is_bitwise_and_deterministic(torch_cuda):
             assert torch.equal(slab, full[a:b]), (cuts, a, b)
 
 
-def test_bp_walk_variants(torch_cuda, monkeypatch):
+def test_bp_walk_variants(torch_cuda, auto_variant):
     """PAIR walks: the fp32x2 walk on the pair patch (WALK 4), the scalar walk (2) and the RAW
     walk reading the TMA box (5) are bitwise equal, on whole chunks and on partial ones (slab
     cut inside a chunk).  TRIPLE walks: the RAW triple walk (6, the default where
@@ -191,7 +200,7 @@ def test_bp_walk_variants(torch_cuda, monkeypatch):
     partial chunks) are bitwise equal, a slab split under walk 6 is bitwise the whole-volume
     result, and both match the oracle."""
     torch = torch_cuda
-    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject, set_bp_variant
 
     spec = _spec(48, 96, 160, 48, 40, 160)  # dv/dk in [0.60, 0.77]: PAIR and TRIPLE apply
     g = Geometry.from_spec(spec)
@@ -199,7 +208,7 @@ def test_bp_walk_variants(torch_cuda, monkeypatch):
     Q = torch.from_numpy(Qn).cuda()
 
     def run(w, k0=0, nk=spec.Nz):
-        monkeypatch.setenv("IFDK_BP_WALK", w)
+        set_bp_variant(int(w))
         vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
         ifdk_backproject(g, Q, 0, vol, k0=k0)
         torch.cuda.synchronize()
@@ -219,12 +228,12 @@ def test_bp_walk_variants(torch_cuda, monkeypatch):
     assert_parity(run("4").cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, "bp pair walk")
 
 
-def test_bp_three_row_triple_walk(torch_cuda, monkeypatch):
+def test_bp_three_row_triple_walk(torch_cuda, auto_variant):
     """dv/dk < 1/2 (config 5's regime): the 3-row TRIPLE RAW walk (7, the default there) and its
     pair-patch companion (8, partial chunks) are bitwise equal, slab splits are bitwise the
     whole-volume result, and the result matches the oracle."""
     torch = torch_cuda
-    from paper_1909_02724_b200 import Geometry, ifdk_backproject
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject, set_bp_variant
 
     spec = _spec(48, 96, 96, 48, 40, 200)  # dv/dk in [0.29, 0.37]
     g = Geometry.from_spec(spec)
@@ -232,7 +241,7 @@ def test_bp_three_row_triple_walk(torch_cuda, monkeypatch):
     Q = torch.from_numpy(Qn).cuda()
 
     def run(w, k0=0, nk=spec.Nz):
-        monkeypatch.setenv("IFDK_BP_WALK", w)
+        set_bp_variant(int(w))
         vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
         ifdk_backproject(g, Q, 0, vol, k0=k0)
         torch.cuda.synchronize()
@@ -468,3 +477,41 @@ def test_bp_random_geometries(torch_cuda, seed):
     og = oracle.OracleGeometry(**spec.geometry_args())
     ref = oracle.backproject_volume(og, Q.astype(np.float64), s0=s0, k0=k0, nk=nk)
     assert_parity(vol.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, f"bp random geometry {seed}")
+
+
+@pytest.mark.parametrize("family,walks,dims", [
+    ("4-row TRIPLE", ("6", "3"), (48, 96, 256, 48, 40, 256)),   # dv/dk in [0.60, 0.77]
+    ("3-row TRIPLE", ("7", "8"), (48, 96, 120, 48, 40, 256)),   # dv/dk in [0.28, 0.36]
+    ("PAIR", ("5", "4", "2"), (48, 96, 192, 48, 40, 256)),      # dv/dk in [0.45, 0.58]
+])
+def test_bp_partial_chunks_far_into_the_chunk(torch_cuda, auto_variant, family, walks, dims):
+    """Slab cuts deep inside a 64-slice chunk (k0 % 64 in {57, 59, 63}, ends 1, 3, 5 slices
+    into the next chunk): the partial-chunk walks run the whole unrolled walk with masked
+    slices whose floors lie outside the staged box; their shared loads are clamped into it
+    (backproject.cu clamp_floor).  Every variant of the family is bitwise the
+    whole-volume result, which matches the oracle.  Run under compute-sanitizer by
+    tools/gpu_sanitize.sh."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject, set_bp_variant
+
+    spec = _spec(*dims)
+    g = Geometry.from_spec(spec)
+    Qn = _oracle_Q32(spec, _phantom_E(spec))
+    Q = torch.from_numpy(Qn).cuda()
+
+    def run(w, k0=0, nk=spec.Nz):
+        set_bp_variant(int(w))
+        lo = min(g.band_rows(k0, nk, s)[0] for s in range(spec.Np))
+        hi = max(g.band_rows(k0, nk, s)[1] for s in range(spec.Np))
+        vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
+        ifdk_backproject(g, Q[:, lo:hi + 1].contiguous(), 0, vol, k0=k0, v0=lo)
+        torch.cuda.synchronize()
+        return vol
+
+    whole = run(walks[0])
+    for w in walks:
+        for k0, k1 in ((57, 65), (59, 131), (63, 197), (121, 128), (64, 69), (185, 256)):
+            assert torch.equal(run(w, k0, k1 - k0), whole[k0:k1]), (family, w, k0, k1)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
+    assert_parity(whole.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, f"bp {family} partial chunks")
