@@ -9,8 +9,8 @@ synthetic Shepp-Logan projections (BASELINE.json configs; default config 4:
 (N_x N_y N_z N_p / (T 2^30)) for the whole step plus its end-to-end
 seconds.  N > 1 runs the k-slab split (dist.kslab_reconstruct) under torchrun:
 every rank filters its own views, the filter stores each row band straight into the
-ranks that need it (symmetric memory over NVLink; `--exchange nccl`: an NCCL
-all-to-all), each rank back-projects its slab; the step time is the max over ranks
+ranks that need it (CUDA-IPC peer memory over NVLink with device-side signals;
+`--exchange nccl`: an NCCL all-to-all), each rank back-projects its slab; the step time is the max over ranks
 (CUDA events + barrier).  `--impl reference` times the fp64 CPU oracle (oracle/) on a
 bounded sample.
 
@@ -50,8 +50,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl"],
-                    help="k-slab band exchange: fused filter + NVLink scatter (auto) or NCCL")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="k-slab band exchange: fused filter + peer-memory scatter (auto/p2p) "
+                         "or NCCL all-to-all")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip timing configs 1-3 at N = 1")
     ap.add_argument("--no-iterative", action="store_true",
@@ -267,6 +268,37 @@ def _max_over_ranks(x, world, dev):
     return float(t.item())
 
 
+def kslab_cross_check(g, spec, vol, k0, nk, ell, dev):
+    """Max |slab - recomputation| / max |recomputation| over the first and last 64 slices of
+    the slab k0..k0+nk-1 (see run_ours)."""
+    import torch
+
+    import synth
+    from paper_1909_02724_b200 import ifdk_backproject, ifdk_filter
+    from paper_1909_02724_b200.dist import band_union
+
+    worst, checked = 0.0, []
+    for a in sorted({k0, max(k0, k0 + nk - 64)}):
+        m = min(64, k0 + nk - a)
+        lo, hi = band_union(g, a, m, 0, spec.Np)
+        E = torch.empty((spec.Np, hi - lo + 1, spec.Nu), device=dev)
+        synth.project_gpu(spec.Nu, spec.Nv, spec.Du, spec.Dv, spec.D, spec.d, spec.theta, ell, 0,
+                          spec.Np, lo, hi - lo + 1, E.data_ptr(),
+                          torch.cuda.current_stream().cuda_stream)
+        ifdk_filter(g, E, E, v0=lo)
+        ref = torch.empty((m, spec.Ny, spec.Nx), device=dev)
+        ifdk_backproject(g, E, 0, ref, k0=a, v0=lo)
+        d = float((vol[a - k0:a - k0 + m] - ref).abs().max() / ref.abs().max().clamp_min(1e-30))
+        worst = max(worst, d)
+        checked.append([a, m])
+        del E, ref
+    torch.cuda.empty_cache()
+    return {"slices": checked, "max_rel_diff": worst, "tolerance": 1e-5,
+            "ok": worst <= 1e-5,
+            "what": "each rank's first / last 64 slices vs an exchange-free recomputation "
+                    "(own row band generated on the device, filter + BP on this GPU)"}
+
+
 def run_ours(args, spec, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -437,6 +469,18 @@ def run_ours(args, spec, rank, world, local_rank):
     if use_kslab and stage.get("wall_ms"):
         # delta: sum of the stage times over the wall time of the pipelined step
         stage["delta"] = (stage.get("filter_pack_ms", 0) + stage.get("bp_ms", 0)) / stage["wall_ms"]
+
+    # At N > 1 (or the forced k-slab path) every rank cross-checks the first and last 64
+    # slices of its slab against an exchange-free recomputation: the detector row band those
+    # slices need, generated on the device for all views, filtered and back-projected by this
+    # GPU alone.  A band routed to the wrong rank or offset would show as a gross error; the
+    # filter pairs rows differently, so equality is to fp32 rounding, not bitwise.  (bench.py
+    # runs the fp64 oracle only in its cpu_baseline leg; the oracle parity of this driver is
+    # tests/test_gpu_dist.py.)
+    slab_check = None
+    if use_kslab:
+        slab_check = kslab_cross_check(g, spec, vol, k0, nk, ell, dev)
+        slab_check["max_rel_diff"] = _max_over_ranks(slab_check["max_rel_diff"], world, dev)
 
     # End to end through the public API: H2D of the raw projections from pinned host memory
     # and D2H of the volume inside the timed region, every step.
@@ -739,6 +783,8 @@ def run_ours(args, spec, rank, world, local_rank):
     }
     if stage:
         out["stage_ms"] = stage
+    if slab_check:
+        out["slab_cross_check"] = slab_check
     if variants:
         out["variants"] = variants
     if others:

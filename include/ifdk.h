@@ -147,9 +147,10 @@ ifdk_status ifdk_signal(int n_flags, unsigned int* const* flags, void* stream);
 /* Later work on `stream` waits until each of the n consecutive device words at
  * flags_dev (local memory) has reached `target` (compared modulo 2^32, so the
  * counters may wrap), read with ld.acquire.sys.  A word that never reaches the target
- * (a dead peer) traps after 300 s instead of hanging the GPU.
+ * (a dead peer) traps after timeout_ms (0: 300 s) instead of hanging the GPU.
  * Errors: INVALID_ARGUMENT (NULL, n outside 1..1024). */
-ifdk_status ifdk_wait(const unsigned int* flags_dev, int n, unsigned int target, void* stream);
+ifdk_status ifdk_wait(const unsigned int* flags_dev, int n, unsigned int target,
+                      unsigned int timeout_ms, void* stream);
 
 /* Alg. alg:bp + alg:subpixel for views s0..s0+n_views-1 into the
  * slab k0..k0+nk-1:  vol_dev[k-k0][j][i] (=|+=) sum_s f^2 . interp2(Q_s, u, v).

@@ -1310,6 +1310,46 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
 
 }  // namespace
 
+// Lazy module loading loads a kernel at its first launch, which waits for the context to go
+// idle: a kernel that spins on a peer's signal (ifdk_wait) would then deadlock against the
+// first launch of any kernel behind it.  ifdk_wait calls this first (cudaFuncGetAttributes
+// loads the function).
+template <typename K>
+static void touch_kernel(K k)
+{
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(k)) != cudaSuccess)
+        cudaGetLastError();
+}
+
+template <int P2>
+static void preload_bp_p2()
+{
+    touch_kernel(bp_kernel<64, P2, true, 2>);
+    touch_kernel(bp_kernel<64, P2, true, 3>);
+    touch_kernel(bp_kernel<64, P2, true, 4>);
+    touch_kernel(bp_kernel<64, P2, true, 8>);
+    touch_kernel(bp_kernel<32, P2, true, 2>);
+    touch_kernel(bp_kernel<32, P2, true, 1>);
+    touch_kernel(bp_kernel<64, P2, false, 2>);
+    touch_kernel(bp_kernel<32, P2, false, 2>);
+    touch_kernel(bp_kernel<32, P2, false, 1>);
+}
+
+void preload_bp_kernels()
+{
+    preload_bp_p2<24>();
+    preload_bp_p2<40>();
+    preload_bp_p2<56>();
+    preload_bp_p2<72>();
+    touch_kernel(bp_raw_kernel<64, 40, 0>);
+    touch_kernel(bp_raw_kernel<64, 72, 0>);
+    touch_kernel(bp_raw_kernel<64, 40, 1>);
+    touch_kernel(bp_raw_kernel<64, 72, 1>);
+    touch_kernel(bp_raw_kernel<64, 40, 2>);
+    touch_kernel(bp_raw_kernel<64, 72, 2>);
+}
+
 void set_bp_variant(int walk, int raster)
 {
     g_walk_override.store(walk, std::memory_order_relaxed);

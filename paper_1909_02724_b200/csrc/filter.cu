@@ -503,6 +503,23 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
 
 }  // namespace
 
+void preload_filter_kernels()  // see preload_bp_kernels (backproject.cu)
+{
+    cudaFuncAttributes a;
+    const void* ks[] = {
+        reinterpret_cast<const void*>(filter_fft_kernel),
+        reinterpret_cast<const void*>(filter_f4k_kernel<true, 1>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<false, 1>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<true, 2>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<false, 2>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<true, 4>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<false, 4>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<true, 8>),
+        reinterpret_cast<const void*>(filter_f4k_kernel<false, 8>)};
+    for (const void* k : ks)
+        if (cudaFuncGetAttributes(&a, k) != cudaSuccess) cudaGetLastError();
+}
+
 ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n_views, int v0,
                           int n_rows, cudaStream_t st, int n_dest, const ifdk_band_dest* dests,
                           const PeerFlags* flags)

@@ -71,6 +71,10 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
 // peer.cu: flags[i] += 1 after all earlier work on the stream
 ifdk_status launch_signal(const PeerFlags& f, cudaStream_t st);
 
+// Force-load (lazy module loading) every kernel that can run while a wait kernel spins.
+void preload_filter_kernels();
+void preload_bp_kernels();
+
 // backproject.cu
 ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,

@@ -16,6 +16,7 @@
 //    stream-ordered after the back-projection that read the buffer; a kernel completes only
 //    after all its loads have returned, so no later store can be observed by them.
 #include <cstring>
+#include <mutex>
 
 #include "ifdk_internal.h"
 
@@ -136,13 +137,40 @@ extern "C" ifdk_status ifdk_signal(int n_flags, unsigned int* const* flags, void
     return launch_signal(f, (cudaStream_t)stream);
 }
 
+// Under lazy module loading (the CUDA 12 default) a kernel is loaded at its first launch, and
+// loading waits for the context to be idle: a wait kernel spinning for a signal that a
+// not-yet-loaded kernel (a peer's scatter, this GPU's own next filter) will send would never
+// finish.  So every kernel of the exchange pipeline is loaded before the first wait kernel
+// is launched on a device.
+static void preload_once()
+{
+    static std::mutex mu;
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+        cudaGetLastError();
+        return;
+    }
+    std::lock_guard<std::mutex> lk(mu);
+    if (done[dev]) return;
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(signal_kernel)) != cudaSuccess ||
+        cudaFuncGetAttributes(&a, reinterpret_cast<const void*>(wait_kernel)) != cudaSuccess)
+        cudaGetLastError();
+    preload_filter_kernels();
+    preload_bp_kernels();
+    done[dev] = true;
+}
+
 extern "C" ifdk_status ifdk_wait(const unsigned int* flags_dev, int n, unsigned int target,
-                                 void* stream)
+                                 unsigned int timeout_ms, void* stream)
 {
     if (!flags_dev || n < 1 || n > 1024)
         return fail(IFDK_ERR_INVALID_ARGUMENT, "need flags and 1 <= n <= 1024");
-    wait_kernel<<<1, ((n + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(flags_dev, n, target,
-                                                                      kWaitTimeoutNs);
+    preload_once();
+    const unsigned long long ns =
+        timeout_ms ? 1000000ull * timeout_ms : kWaitTimeoutNs;
+    wait_kernel<<<1, ((n + 31) / 32) * 32, 0, (cudaStream_t)stream>>>(flags_dev, n, target, ns);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "wait_kernel launch");
     count_launch();

@@ -187,12 +187,14 @@ def plan_exchange(g, plan: SlabPlan, rank: int, t: int) -> Exchange:
 class _Streams:
     """CUDA streams/events for the pipeline, or no-ops for CPU tensors (gloo tests)."""
 
-    def __init__(self, cuda: bool):
+    def __init__(self, cuda: bool, streams=None):
         import torch
 
         self.cuda = cuda
         self.torch = torch
-        if cuda:
+        if cuda and streams is not None:
+            self.F, self.B, self.C = streams
+        elif cuda:
             self.F = torch.cuda.Stream()  # filter + band packing (+ exchange issue)
             self.B = torch.cuda.Stream()  # back-projection
             self.C = torch.cuda.Stream()  # host copies
@@ -250,6 +252,10 @@ class PeerExchange:
         self.recv_max = list(recv_max)
         self._own, self._opened = list(own), list(opened)
         self.kind = "p2p-fused"
+        # rounds of earlier pipeline calls: the signal words count on from there (every rank
+        # runs the same calls with the same number of rounds)
+        self.rounds_done = 0
+        self.timeout_ms = 0  # of the wait kernels (0: the library's 300 s)
 
     # -- construction
     @staticmethod
@@ -313,11 +319,13 @@ class PeerExchange:
 
     # -- the round protocol (each call enqueues on the current stream)
     def wait_free(self, t):
-        """Before scattering round t: every rank has released buffer t % 2 (round t - 2)."""
+        """Before scattering round t: every rank has released buffer t % 2 (round t - 2 of
+        this call, or every round of the earlier calls)."""
         from .ifdk import ifdk_wait
 
-        if t >= 2:
-            ifdk_wait(self.bases[self.rank] + 256, self.world, t - 1)
+        target = self.rounds_done + (t - 1 if t >= 2 else 0)
+        if target > 0:
+            ifdk_wait(self.bases[self.rank] + 256, self.world, target, self.timeout_ms)
 
     def scatter(self, g, src, q, bands, filter_fn=None):
         """Filter src (the rank's block of this round, None if it has none) into every
@@ -336,7 +344,7 @@ class PeerExchange:
     def wait_landed(self, t):
         from .ifdk import ifdk_wait
 
-        ifdk_wait(self.bases[self.rank], self.world, t + 1)
+        ifdk_wait(self.bases[self.rank], self.world, self.rounds_done + t + 1, self.timeout_ms)
 
     def release(self):
         """After back-projecting a round: tell every rank its buffer here may be reused."""
@@ -362,7 +370,8 @@ def _peer_exchange(group, rank, world, recv_max, dev):
         ex = PeerExchange.create(group, rank, world, recv_max)
     except Exception as exc:  # noqa: BLE001 -- no peer mapping: the NCCL band exchange
         err = exc
-    ok = torch.tensor([1 if ex is not None else 0], device=dev)
+    on_dev = dist.get_backend(group) == "nccl"
+    ok = torch.tensor([1 if ex is not None else 0], device=dev if on_dev else "cpu")
     dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
     if int(ok.item()) == 0:
         import warnings
@@ -383,7 +392,7 @@ def _peer_exchange(group, rank, world, recv_max, dev):
 
 def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, timings,
               raw_local=None, raw_host=None, vol_host=None, force_exchange=False,
-              exchange="auto", peer=None):
+              exchange="auto", peer=None, streams=None):
     import torch
     import torch.distributed as dist
 
@@ -394,7 +403,7 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
     xchg = world > 1 or (force_exchange and dist.is_available() and dist.is_initialized())
     k0, nk = plan.slab(rank)
     cuda = vol_slab.is_cuda
-    S = _Streams(cuda)
+    S = _Streams(cuda, streams)
     dev = vol_slab.device
     Nv, Nu = g.Nv, g.Nu
     rounds = plan.n_rounds
@@ -416,6 +425,11 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
             raise RuntimeError("exchange='p2p': peer memory unavailable")
     if not xchg:
         peer = None
+    if peer is not None and cuda:
+        # the one torch kernel the pipeline may launch (zero_ of untouched slices), loaded now:
+        # under lazy module loading a first launch behind a spinning wait kernel would
+        # deadlock (csrc/peer.cu preloads the library's own kernels the same way)
+        torch.zeros(1, device=dev)
     nbuf = min(2, rounds)
     if peer is not None:
         Qbuf = [None] * nbuf
@@ -573,6 +587,8 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
             b_marks.append((b0, b1))
             ev_bp_done[q] = S.event()
             S.record(ev_bp_done[q], S.B)
+    if peer is not None:
+        peer.rounds_done += rounds
     if rounds == 0 and nk > 0:  # no views at all
         vol_slab.zero_()
         if vol_host is not None:
@@ -601,30 +617,32 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
 def kslab_reconstruct(g, raw_local, vol_slab, plan: SlabPlan, rank: int, group=None,
                       filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
                       timings: Optional[dict] = None, force_exchange: bool = False,
-                      exchange: str = "auto", peer: Optional[PeerExchange] = None):
+                      exchange: str = "auto", peer: Optional[PeerExchange] = None,
+                      streams=None):
     """k-slab FDK on one rank.  raw_local: [plan.n_local(rank)][Nv][Nu], the rank's blocks
     (plan.local_views(rank)) in order, device-resident; vol_slab: [nk][Ny][Nx] (slab
     plan.slab(rank)), overwritten.  Enqueued on side streams that the current stream joins.
     exchange: "auto" fuses the band exchange into the filter over peer (NVLink) memory when
     every rank can map its peers (PeerExchange: ifdk_filter_scatter + device-side signals),
     else NCCL all-to-all; "p2p" requires the fused exchange; "nccl" forces the all-to-all.
-    peer: an existing PeerExchange (e.g. PeerExchange.local for virtual ranks on one GPU)."""
+    peer: an existing PeerExchange (e.g. PeerExchange.local for virtual ranks on one GPU);
+    streams: (filter, back-projection, copy) streams to use instead of three new ones."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
                      raw_local=raw_local, force_exchange=force_exchange, exchange=exchange,
-                     peer=peer)
+                     peer=peer, streams=streams)
 
 
 def kslab_reconstruct_host(g, raw_host, vol_slab, vol_host, plan: SlabPlan, rank: int,
                            group=None, filter_fn: Optional[Callable] = None,
                            bp_fn: Optional[Callable] = None, timings: Optional[dict] = None,
                            force_exchange: bool = False, exchange: str = "auto",
-                           peer: Optional[PeerExchange] = None):
+                           peer: Optional[PeerExchange] = None, streams=None):
     """End-to-end k-slab FDK on one rank: raw_host (pinned, the rank's blocks in order) is
     copied block by block one round ahead; vol_slab (device scratch [nk][Ny][Nx]) is
     streamed to vol_host (pinned) in sub-slabs during the last round."""
     return _pipeline(g, plan, rank, vol_slab, group, filter_fn, bp_fn, timings,
                      raw_host=raw_host, vol_host=vol_host, force_exchange=force_exchange,
-                     exchange=exchange, peer=peer)
+                     exchange=exchange, peer=peer, streams=streams)
 
 
 # ----------------------------------------------------------------------------- R x C grid

@@ -98,7 +98,7 @@ _lib.ifdk_peer_free.argtypes = [_vp]
 _lib.ifdk_peer_free.restype = _i
 _lib.ifdk_signal.argtypes = [_i, ctypes.POINTER(_vp), _vp]
 _lib.ifdk_signal.restype = _i
-_lib.ifdk_wait.argtypes = [_vp, _i, ctypes.c_uint, _vp]
+_lib.ifdk_wait.argtypes = [_vp, _i, ctypes.c_uint, ctypes.c_uint, _vp]
 _lib.ifdk_wait.restype = _i
 _lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp]
 _lib.ifdk_backproject.restype = _i
@@ -266,9 +266,11 @@ def ifdk_signal(flags, stream=None) -> None:
     _check(_lib.ifdk_signal(len(flags), _ptr_array(flags), _stream_ptr(stream)))
 
 
-def ifdk_wait(flags_ptr: int, n: int, target: int, stream=None) -> None:
-    """Later work on the stream waits until the n uint32 words at flags_ptr reach target."""
-    _check(_lib.ifdk_wait(int(flags_ptr), int(n), int(target) & 0xFFFFFFFF, _stream_ptr(stream)))
+def ifdk_wait(flags_ptr: int, n: int, target: int, timeout_ms: int = 0, stream=None) -> None:
+    """Later work on the stream waits until the n uint32 words at flags_ptr reach target
+    (a trap after timeout_ms, 0 = 300 s)."""
+    _check(_lib.ifdk_wait(int(flags_ptr), int(n), int(target) & 0xFFFFFFFF, int(timeout_ms),
+                          _stream_ptr(stream)))
 
 
 class DeviceArray:

@@ -62,3 +62,6 @@ def test_gpu_arm_json_line_single_and_kslab():
     d = _last_json(r.stdout)
     assert BASE_KEYS <= set(d) and d["value"] > 0
     assert "k-slab" in d["config"]["parallelism"]
+    # the k-slab result cross-checked against an exchange-free recomputation, delta reported
+    assert d["slab_cross_check"]["ok"], d["slab_cross_check"]
+    assert d["stage_ms"]["delta"] > 0

@@ -100,9 +100,12 @@ class HostPeerExchange:
                 raise TimeoutError(f"rank {self.rank}: signal row {row} never reached {target}")
             self._time.sleep(0.0005)
 
+    rounds_done = 0  # as dist.PeerExchange: the words count on across pipeline calls
+
     def wait_free(self, t):
-        if t >= 2:
-            self._wait(1, t - 1)
+        target = self.rounds_done + (t - 1 if t >= 2 else 0)
+        if target > 0:
+            self._wait(1, target)
 
     def scatter(self, g, src, q, bands, filter_fn):
         if src is not None and bands:
@@ -117,7 +120,7 @@ class HostPeerExchange:
             self.words[h][0, self.rank] += 1
 
     def wait_landed(self, t):
-        self._wait(0, t + 1)
+        self._wait(0, self.rounds_done + t + 1)
 
     def recv(self, q, off, rn, rows, Nu):
         a = q * self.recv_max[self.rank] + off
@@ -155,8 +158,11 @@ def _worker(rank, world, port, mode, out_q):
                 rmax = [max(sum(e.recv_sizes) for e in exchanges(g, plan, h)) for h in range(world)]
                 peer = HostPeerExchange(f"ifdk_{port}", rank, world, rmax)
                 try:
-                    kslab_reconstruct(g, torch.from_numpy(mine), vol, plan, rank, filter_fn=f,
-                                      bp_fn=b, peer=peer)
+                    for _ in range(2):  # the second call counts on from the first's signals
+                        vol.fill_(float("nan"))
+                        kslab_reconstruct(g, torch.from_numpy(mine), vol, plan, rank,
+                                          filter_fn=f, bp_fn=b, peer=peer)
+                    assert peer.rounds_done == 2 * plan.n_rounds
                 finally:
                     peer.close()
             else:

@@ -22,7 +22,7 @@ int main()
     CK(cuInit(0));
     CUdevice dev;
     CK(cuDeviceGet(&dev, 0));
-    int mc = 0, fab = 0;
+    int mc = 0;
     CK(cuDeviceGetAttribute(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
     printf("MULTICAST_SUPPORTED=%d\n", mc);
     cudaSetDevice(0);
@@ -31,20 +31,32 @@ int main()
     const size_t n = 1 << 20;
     CUmulticastObjectProp prop = {};
     prop.numDevices = 1;
-    prop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     prop.size = n * 4;
     size_t gran = 0;
-    CK(cuMulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-    prop.size = (n * 4 + gran - 1) / gran * gran;
-    printf("granularity=%zu size=%zu\n", gran, prop.size);
     CUmemGenericAllocationHandle mch;
-    CK(cuMulticastCreate(&mch, &prop));
+    CUmemAllocationHandleType types[3] = {CU_MEM_HANDLE_TYPE_NONE, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                          CU_MEM_HANDLE_TYPE_FABRIC};
+    bool made = false;
+    for (auto ht : types) {
+        prop.handleTypes = ht;
+        prop.size = n * 4;
+        if (cuMulticastGetGranularity(&gran, &prop, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS) {
+            printf("handle type %d: granularity query failed\n", (int)ht);
+            continue;
+        }
+        prop.size = (n * 4 + gran - 1) / gran * gran;
+        CUresult r = cuMulticastCreate(&mch, &prop);
+        const char* es; cuGetErrorString(r, &es);
+        printf("handle type %d: granularity=%zu size=%zu create: %s\n", (int)ht, gran, prop.size, es);
+        if (r == CUDA_SUCCESS) { made = true; break; }
+    }
+    if (!made) return 0;
     CK(cuMulticastAddDevice(mch, dev));
     CUmemAllocationProp ap = {};
     ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
     ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     ap.location.id = 0;
-    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    ap.requestedHandleTypes = (CUmemAllocationHandleType)prop.handleTypes;
     CUmemGenericAllocationHandle mh;
     CK(cuMemCreate(&mh, prop.size, &ap, 0));
     CK(cuMulticastBindMem(mch, 0, mh, 0, prop.size, 0));
