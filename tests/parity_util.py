@@ -26,3 +26,31 @@ def assert_parity(got, ref, rmse_tol, max_tol, what=""):
     print(f"PARITY {what}: relRMSE {r:.3e}  max|d|/max|ref| {m:.3e}  (n={np.size(ref)})")
     assert r <= rmse_tol and m <= max_tol, f"{what}: relRMSE {r:.3e} (tol {rmse_tol}), max|d|/max|ref| {m:.3e} (tol {max_tol})"
     return r, m
+
+
+_POOL = None
+
+
+def filter_fft_threads(og, E, v0=0):
+    """oracle.filter_fft over row ranges on host threads (rows are independent in Alg.
+    alg:filter, so the values are bitwise those of one call)."""
+    import concurrent.futures as cf
+    import os
+
+    import oracle
+
+    global _POOL
+    nt = os.cpu_count() or 1
+    if _POOL is None:
+        _POOL = cf.ThreadPoolExecutor(nt)
+    n_rows = E.shape[1]
+    parts = min(n_rows, 2 * nt)
+    cuts = [n_rows * i // parts for i in range(parts + 1)]
+    Q = np.empty(E.shape, np.float64)
+
+    def job(a, b):
+        Q[:, a:b] = oracle.filter_fft(og, E[:, a:b], v0=v0 + a, workers=1)
+
+    for f in [_POOL.submit(job, a, b) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]:
+        f.result()
+    return Q

@@ -366,6 +366,8 @@ def test_reconstruct_host_equals_device(torch_cuda, shape):
     vol_h = np.empty(shape, np.float32)
     ifdk_reconstruct_host(g, E, vol_h)
     assert np.array_equal(vol_h, vol_d.cpu().numpy())
+    ref = oracle.reconstruct(oracle.OracleGeometry(**spec.geometry_args()), E, fft=True)
+    assert_parity(vol_h, ref, VOL_RMSE, VOL_MAX_REL, f"ifdk_reconstruct_host 300 views {shape}")
 
 
 @pytest.mark.parametrize("shape,cuts", [((600, 24, 40), (0, 64, 300, 576, 600)),
@@ -385,11 +387,44 @@ def test_reconstruct_slab_host_zero_exchange(torch_cuda, shape, cuts):
     vol_d = torch.empty(shape, device="cuda")
     ifdk_reconstruct(g, torch.from_numpy(E).cuda(), vol_d)
     full = vol_d.cpu().numpy()
+    ref = oracle.reconstruct(oracle.OracleGeometry(**spec.geometry_args()), E, fft=True)
+    got = np.empty(shape, np.float32)
     for a, b in zip(cuts[:-1], cuts[1:]):
         slab = np.empty((b - a, Ny, Nx), np.float32)
         ifdk_reconstruct_slab_host(g, E, a, slab)
         d = slab.astype(np.float64) - full[a:b]
         assert np.abs(d).max() <= 1e-5 * np.abs(full).max(), (a, b, np.abs(d).max())
+        got[a:b] = slab
+    assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL,
+                  f"ifdk_reconstruct_slab_host 300 views {shape} slabs {cuts}")
+
+
+def test_host_entry_points_config1_vs_oracle(torch_cuda):
+    """Config 1 through every public end-to-end entry point, each against the oracle:
+    ifdk_reconstruct_host, ifdk_reconstruct_slab_host (two slabs) and kslab_reconstruct_host."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_reconstruct_host, ifdk_reconstruct_slab_host
+    from paper_1909_02724_b200.dist import SlabPlan, kslab_reconstruct_host
+
+    spec = synth.config(1)
+    g = Geometry.from_spec(spec)
+    E = _phantom_E(spec)
+    ref = oracle.reconstruct(oracle.OracleGeometry(**spec.geometry_args()), E)
+    vol_h = np.full((64, 64, 64), np.nan, np.float32)
+    ifdk_reconstruct_host(g, E, vol_h)
+    assert_parity(vol_h, ref, VOL_RMSE, VOL_MAX_REL, "config 1 ifdk_reconstruct_host")
+    slabs = np.full((64, 64, 64), np.nan, np.float32)
+    for a, b in ((0, 40), (40, 64)):
+        part = np.empty((b - a, 64, 64), np.float32)
+        ifdk_reconstruct_slab_host(g, E, a, part)
+        slabs[a:b] = part
+    assert_parity(slabs, ref, VOL_RMSE, VOL_MAX_REL, "config 1 ifdk_reconstruct_slab_host")
+    raw_h = torch.from_numpy(E).pin_memory()
+    vol_k = torch.full((64, 64, 64), float("nan")).pin_memory()
+    vol_d = torch.empty((64, 64, 64), device="cuda")
+    kslab_reconstruct_host(g, raw_h, vol_d, vol_k, SlabPlan(1, 64, 64), 0)
+    torch.cuda.synchronize()
+    assert_parity(vol_k.numpy(), ref, VOL_RMSE, VOL_MAX_REL, "config 1 kslab_reconstruct_host")
 
 
 def test_synth_gpu_generator_matches_cpu(torch_cuda):
@@ -431,6 +466,9 @@ def test_kslab_driver_single_rank_equals_reconstruct(torch_cuda):
     kslab_reconstruct_host(g, raw_h, vol2, vol_h, plan1, 0)
     torch.cuda.synchronize()
     assert torch.equal(vol_h, ref.cpu())
+    oref = oracle.reconstruct(oracle.OracleGeometry(**spec.geometry_args()), raw_h.numpy(),
+                              fft=True)
+    assert_parity(vol_h.numpy(), oref, VOL_RMSE, VOL_MAX_REL, "kslab_reconstruct_host 600 views")
     Q = torch.empty_like(raw)
     ifdk_filter(g, raw, Q)
     for world in (2, 4):
