@@ -35,7 +35,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SMEM_BYTES_PER_UPDATE = 16  # 4 bilinear taps x 4 B (Alg. alg:subpixel), DESIGN.md "Roofline"
+SMEM_BYTES_PER_UPDATE = 16  # 4 bilinear taps x 4 B (Alg. alg:subpixel), SURVEY 8(d)'s figure
 SMEM_B_PER_CLK_PER_SM = 128
 N_SM = 148
 
@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-oracle-full", action="store_true",
+                    help="skip the full config-2 oracle run (~70 s on 16 cores) in cpu_baseline")
     ap.add_argument("--exchange", default="auto", choices=["auto", "p2p", "nccl"],
                     help="k-slab band exchange: fused filter + peer-memory scatter (auto/p2p) "
                          "or NCCL all-to-all")
@@ -160,6 +162,23 @@ def ncu_field(config: int, key: str):
             e = json.load(f).get(str(config))
         return e.get(key) if e else None
     return None
+
+
+def walk_smem_bytes(spec):
+    """Algorithmic shared-memory bytes per update of the k-walk the library picks for the
+    geometry: per 64-slice chunk and view a thread issues LDS.32 taps --
+    4-row TRIPLE (0.5 <= dv/dk): ten 3+3-slice groups x 16 taps + a 4-slice PAIR quad x 12 taps
+    = 688 B / 64 updates = 10.75 B; 3-row TRIPLE (dv/dk < 0.5): 10 x 12 + 12 taps = 8.25 B;
+    PAIR: 12 taps per 4 updates = 12 B."""
+    import math
+
+    r = math.hypot(spec.Nx * spec.Dx, spec.Ny * spec.Dy) / 2
+    dv = [spec.D / spec.Dv * spec.Dz / z for z in (spec.d + r, spec.d - r)]
+    if min(dv) >= 0.5001:
+        return 10.75, "4-row TRIPLE"
+    if max(dv) < 0.4999:
+        return 8.25, "3-row TRIPLE"
+    return 12.0, "PAIR"
 
 
 def smem_probe():
@@ -422,7 +441,9 @@ def run_ours(args, spec, rank, world, local_rank):
         bp_s = stage.get("bp_ms", float("nan")) / 1e3 / max(plan.n_rounds, 1)
         upd_per_launch = spec.Nx * spec.Ny * nk * spec.Np / max(plan.n_rounds, 1)
         bp_share = stage.get("bp_ms", float("nan")) / ms
-    achieved_gbs = SMEM_BYTES_PER_UPDATE * upd_per_launch / bp_s / 1e9
+    walk_b, walk_name = walk_smem_bytes(spec)
+    achieved_gbs = walk_b * upd_per_launch / bp_s / 1e9
+    achieved_4tap_gbs = SMEM_BYTES_PER_UPDATE * upd_per_launch / bp_s / 1e9
     hbm_peak = float(measured_peaks().get("hbm_gbs", 6543.4))
     # BP against HBM: algorithmic bytes of one launch = its filtered views read once + the
     # slab written (first launch) or read and written (accumulating launches): 8 B per voxel
@@ -431,7 +452,7 @@ def run_ours(args, spec, rank, world, local_rank):
     bp_hbm_bytes = 4 * views_per_launch * spec.Nu * spec.Nv + 8 * spec.Nx * spec.Ny * nk
     roofline_hbm = {"bound": "hbm", "achieved": bp_hbm_bytes / bp_s / 1e9, "peak": hbm_peak,
                     "unit": "GB/s", "frac": bp_hbm_bytes / bp_s / 1e9 / hbm_peak,
-                    "kernel": "bp_raw_kernel (4 B per filtered pixel + 8 B per voxel per launch)",
+                    "kernel": "bp_tmem2_kernel (4 B per filtered pixel + 8 B per voxel per launch)",
                     "peak_basis": "MEASURED_PEAKS.json hbm_gbs"}
     # BP against the issue roofline: SASS instructions per update from the committed ncu
     # capture (profiles/ncu_bp_traffic.json "inst_per_update") x updates/s, against
@@ -445,7 +466,9 @@ def run_ours(args, spec, rank, world, local_rank):
         roofline_issue = {"bound": "issue", "achieved": ach_ti, "peak": peak_ti,
                           "unit": "Tinst/s (thread)", "frac": ach_ti / peak_ti,
                           "inst_per_update": ipu,
-                          "kernel": "bp_raw_kernel", "peak_basis": "148 SM x 4 x 32 x sm_max_mhz"}
+                          "kernel": "bp_tmem2_kernel",
+                          "peak_basis": "148 SM x 4 x 32 x sm_max_mhz; inst_per_update from the "
+                                        "committed ncu capture (profiles/ncu_bp_traffic.json)"}
     filt = None
     if filter_events:
         fdur = sum(a.elapsed_time(b) for a, b, _ in filter_events) / len(filter_events) / 1e3
@@ -730,13 +753,23 @@ def run_ours(args, spec, rank, world, local_rank):
         v, s, desc = oracle_sample(spec, 32, 1 << 25)  # ~10-20 s on the box's 16 cores
         cpu = {"value": v, "unit": "GUPS", "cores": oracle.num_threads(), "kind": "oracle",
                "sample": desc, "seconds": s, "cpu_model": cpu_model()}
-        # config 1 (the case the oracle finishes in seconds) in full: filter + back-projection
-        c1 = synth.config(1)
-        E1 = synth.project(c1.Nu, c1.Nv, c1.Du, c1.Dv, c1.D, c1.d, c1.theta,
-                           synth.default_ellipsoids(c1), 0, c1.Np)
-        t1 = time.perf_counter()
-        oracle.reconstruct(oracle.OracleGeometry(**c1.geometry_args()), E1)
-        cpu["config1_full_seconds"] = time.perf_counter() - t1
+        cpu["updates_per_s_per_core"] = v * 2 ** 30 / cpu["cores"]
+        # configs 1 and 2 in full, not extrapolated: oracle filter (direct sum for
+        # config 1, FFT form for config 2) + back-projection of every voxel over every view
+        for cid, fft in ((1, False), (2, True)):
+            if args.no_oracle_full and cid == 2:
+                continue
+            c = synth.config(cid)
+            Ec = synth.project(c.Nu, c.Nv, c.Du, c.Dv, c.D, c.d, c.theta,
+                               synth.default_ellipsoids(c), 0, c.Np)
+            t1 = time.perf_counter()
+            oracle.reconstruct(oracle.OracleGeometry(**c.geometry_args()), Ec, fft=fft)
+            dt = time.perf_counter() - t1
+            cpu[f"config{cid}_full"] = {"workload": c.name, "seconds": dt,
+                                        "gups": gups(c, dt),
+                                        "updates_per_s_per_core": c.updates / dt / cpu["cores"],
+                                        "measured": "in full (every voxel, every view)"}
+            del Ec
     value = gups(spec, ms / 1e3)
     out = {
         "metric": "fdk_gups",
@@ -771,7 +804,16 @@ def run_ours(args, spec, rank, world, local_rank):
                      "traffic": (ncu_traffic(args.config) * upd_per_launch
                                  / (256.0 * spec.Nx * spec.Ny * spec.Nz)
                                  if ncu_traffic(args.config) else None),
-                     "kernel": "bp_raw_kernel (16 algorithmic B/update of bilinear taps)",
+                     "bytes_per_update": walk_b,
+                     "kernel": f"bp_tmem2_kernel ({walk_name} walk: {walk_b} algorithmic B/update "
+                               "of shared-memory taps; TMEM accumulators, two views per step)",
+                     "smem_bytes_per_update_ncu": ncu_field(args.config, "smem_bytes_per_update"),
+                     "four_tap": {"bytes_per_update": SMEM_BYTES_PER_UPDATE,
+                                  "achieved": achieved_4tap_gbs,
+                                  "frac": achieved_4tap_gbs / peak_gbs,
+                                  "note": "SURVEY 8(d)'s 4-tap figure; the walk reuses detector "
+                                          "rows across slices, so it moves fewer bytes and this "
+                                          "fraction can exceed 1"},
                      "peak_basis": peak_basis},
         "roofline_hbm": roofline_hbm,
         "roofline_issue": roofline_issue,

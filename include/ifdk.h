@@ -169,6 +169,25 @@ ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* filtered_dev, 
                              long n_views, int v0, int n_rows, float* vol_dev, int k0, int nk,
                              int accumulate, void* stream);
 
+/* Fused projection-split back-projection (the paper's single
+ * MPI_Reduce of partial volumes, done inside the back-projection's
+ * write-back instead of a separate reduce-scatter).  Views s0..s0+n_views-1 (filtered_dev
+ * as for ifdk_backproject) are back-projected over slices k0..k0+nk-1, and every 128-view
+ * partial sum of a voxel is ADDED to the destination slab holding its slice: dest[d]
+ * ([..][Ny][Nx] fp32, device memory of this GPU or a peer mapping -- ifdk_peer_open --
+ * reached over NVLink) holds slices dest_k0[d] .. dest_k0[d+1]-1 (the last one through
+ * k0+nk-1).  mode 0: red.global.add.f32 (relaxed, system scope); mode 1:
+ * multimem.red.add.f32, dest[] being multicast mappings (NVLS: the switch adds).  The
+ * caller zeroes the slabs first and orders the adds of all ranks before reading them
+ * (stream / device synchronisation, or ifdk_signal + ifdk_wait).  Sum order across ranks is
+ * not fixed, so results agree with ifdk_backproject to fp32 rounding, not bitwise.
+ * Errors: INVALID_ARGUMENT (NULL, n_dest outside 1..16, mode not 0/1), SHAPE (slab or band
+ * as for ifdk_backproject; dest_k0 not strictly increasing or dest_k0[0] > k0). */
+ifdk_status ifdk_backproject_reduce(const ifdk_geometry* g, const float* filtered_dev, long s0,
+                                    long n_views, int v0, int n_rows, int k0, int nk, int n_dest,
+                                    float* const* dest, const int* dest_k0, int mode,
+                                    void* stream);
+
 /* Whole FDK on device: filter views 0..n_views-1 of raw_dev ([n_views][Nv][Nu])
  * into stream-ordered scratch and back-project them into vol_dev ([Nz][Ny][Nx]),
  * overwriting it.  raw_dev is left unchanged. */
@@ -273,8 +292,10 @@ ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream);
 /* Speed-tuning hook for A/B measurements and tests, not needed in normal use:
  * walk selects the back-projection k-walk among the variants that give BITWISE
  * the same result as the automatic choice for the geometry (PAIR family 2, 4, 5;
- * 4-row TRIPLE family 3, 6 where 0.5 <= dv/dk; 3-row TRIPLE family 7, 8 where
- * dv/dk < 0.5); any other value, or 0, means automatic.
+ * 4-row TRIPLE family 3, 6, 9, 11 where 0.5 <= dv/dk; 3-row TRIPLE family 7, 8,
+ * 10, 12 where dv/dk < 0.5; 9-12 keep the accumulators in tensor memory, 11 / 12
+ * step two views at a time); any other value, or 0, means
+ * automatic.
  * raster sets the CTA raster band in tiles (0 = automatic; >= the tile count =
  * row-major); it only reorders CTAs.  Process-wide; affects later launches. */
 ifdk_status ifdk_set_bp_variant(int walk, int raster);

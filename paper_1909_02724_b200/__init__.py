@@ -11,6 +11,7 @@ from .ifdk import (  # noqa: F401
     IfdkError,
     ifdk_backproject,
     ifdk_backproject_alg2,
+    ifdk_backproject_reduce,
     ifdk_backproject_alg4,
     ifdk_filter,
     ifdk_fill,

@@ -153,6 +153,45 @@ extern "C" ifdk_status ifdk_backproject(const ifdk_geometry* g, const float* fil
                               accumulate, (cudaStream_t)stream);
 }
 
+extern "C" ifdk_status ifdk_backproject_reduce(const ifdk_geometry* g, const float* filtered_dev,
+                                               long s0, long n_views, int v0, int n_rows,
+                                               int k0, int nk, int n_dest, float* const* dest,
+                                               const int* dest_k0, int mode, void* stream)
+{
+    t_launches = 0;
+    if (!g || !dest || !dest_k0 || (!filtered_dev && n_views > 0))
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (mode != 0 && mode != 1) return fail(IFDK_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    if (n_dest < 1 || n_dest > kMaxRedDest)
+        return fail(IFDK_ERR_INVALID_ARGUMENT, "n_dest must be 1..16");
+    ifdk_status s = check_band(g, n_views, v0, n_rows);
+    if (s != IFDK_OK) return s;
+    if (k0 < 0 || nk < 1 || (long)k0 + nk > g->Nz)
+        return fail(IFDK_ERR_SHAPE, "slab k0..k0+nk-1 outside [0, Nz)");
+    // destination slabs: strictly increasing starts, the first at or below k0 (each slab runs
+    // to the next one's start, the last through k0+nk-1)
+    RedDest red;
+    red.mode = mode;
+    red.n = n_dest;
+    for (int d = 0; d < n_dest; ++d) {
+        if (!dest[d]) return fail(IFDK_ERR_INVALID_ARGUMENT, "NULL destination slab");
+        if (d > 0 && dest_k0[d] <= dest_k0[d - 1])
+            return fail(IFDK_ERR_SHAPE, "destination slab starts must increase");
+        red.k0[d] = dest_k0[d];
+        red.base[d] = dest[d];
+    }
+    if (dest_k0[0] > k0) return fail(IFDK_ERR_SHAPE, "destination slabs do not cover k0");
+    for (long t = 0; t < n_views; ++t) {
+        int lo, hi;
+        band_rows(g, k0, nk, s0 + t, &lo, &hi);
+        if (lo <= hi && (lo < v0 || hi > v0 + n_rows - 1))
+            return fail(IFDK_ERR_SHAPE, "the row band does not cover the slab's rows");
+    }
+    if ((s = need_device()) != IFDK_OK) return s;
+    return launch_backproject(g, filtered_dev, s0, n_views, v0, n_rows, nullptr, k0, nk, 1,
+                              (cudaStream_t)stream, &red);
+}
+
 extern "C" ifdk_status ifdk_forward_project(const ifdk_geometry* g, const float* vol_dev, int k0,
                                             int nk, long s0, long n_views, float* proj_dev,
                                             int v0, int n_rows, int accumulate, void* stream)

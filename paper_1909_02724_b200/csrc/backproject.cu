@@ -43,6 +43,7 @@
 
 #include "ifdk_internal.h"
 #include "kwalk.cuh"
+#include "mbar.cuh"
 
 namespace ifdk {
 namespace {
@@ -68,7 +69,40 @@ struct BPParams {
     int pair;            // rows of slack for a multi-slice walk (PAIR / TRIPLE): 1, else 0
     int walk;            // slices per floor: 1, 2 (PAIR) or 3 (TRIPLE)
     int accumulate;
+    // fused reduce (RedDest): 0 = write / accumulate into vol; 1 = red.global.add, 2 =
+    // multimem.red into dest[d] (slices dest_k0[d] ..); vol is unused then
+    int red;
+    int n_dest;
+    int dest_k0[kMaxRedDest];
+    float* dest[kMaxRedDest];
 };
+
+// Address of voxel (i, j, k) in the slab vol (the flush walks it slice by slice).
+__device__ __forceinline__ float* vol_voxel(const BPParams& p, int k, int j, int i)
+{
+    return p.vol + ((long)(k - p.k0) * p.Ny + j) * p.Nx + i;
+}
+
+// One partial sum of voxel (i, j, k) into the volume: q (its address in vol) overwritten /
+// added, or -- the fused reduce -- atomically added into the destination slab holding slice k
+// (slabs need not align with the 64-slice chunks; the order of the adds from different
+// launches / GPUs is not fixed, so fp32 rounding may differ).
+__device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, int j, int i,
+                                          float v, bool overwrite)
+{
+    if (p.red == 0) {
+        *q = overwrite ? v : *q + v;
+        return;
+    }
+    int d = 0;
+    while (d + 1 < p.n_dest && k >= p.dest_k0[d + 1]) ++d;
+    float* r = p.dest[d] + ((long)(k - p.dest_k0[d]) * p.Ny + j) * p.Nx + i;
+    if (p.red == 1)
+        asm volatile("red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(r), "f"(v) : "memory");
+    else
+        asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(r), "f"(v)
+                     : "memory");
+}
 
 struct __align__(16) Meta {
     double P[10];
@@ -77,38 +111,6 @@ struct __align__(16) Meta {
     int fast;            // the patch fits the box
     int pad[3];
 };
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p)
-{
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
-{
-    const uint32_t a = smem_u32(bar);
-    uint32_t ok = 0;
-    do {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}"
-            : "=r"(ok)
-            : "r"(a), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2)
@@ -428,14 +430,14 @@ template <int KC>
 __device__ __forceinline__ void flush_x2(f2x (&acc)[KC / 2], const BPParams& p, int i, int j,
                                          int kb, int kv0, int kv1, bool overwrite)
 {
-    float* q = p.vol + ((long)(kb - p.k0) * p.Ny + j) * p.Nx + i;
+    float* q = vol_voxel(p, kb, j, i);
     long plane = (long)p.Ny * p.Nx;
     asm volatile("mov.b64 %0, %0;" : "+l"(plane));
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
         const f2x a = acc[(kk & ~3) / 2 + (kk & 1)];
         const float v = (kk & 2) ? hi2(a) : lo2(a);
-        if (kk >= kv0 && kk < kv1) *q = overwrite ? v : *q + v;
+        if (kk >= kv0 && kk < kv1) put_voxel(p, q, kb + kk, j, i, v, overwrite);
         q += plane;
     }
 #pragma unroll
@@ -510,13 +512,13 @@ template <int KC>
 __device__ __forceinline__ void flush(float (&acc)[KC], const BPParams& p, int i, int j, int kb,
                                       int kv0, int kv1, bool overwrite)
 {
-    float* q = p.vol + ((long)(kb - p.k0) * p.Ny + j) * p.Nx + i;
+    float* q = vol_voxel(p, kb, j, i);
     long plane = (long)p.Ny * p.Nx;
     // Opaque to the optimiser: stops it from hoisting 64 addresses out of the view loop.
     asm volatile("mov.b64 %0, %0;" : "+l"(plane));
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) {
-        if (kk >= kv0 && kk < kv1) *q = overwrite ? acc[kk] : *q + acc[kk];
+        if (kk >= kv0 && kk < kv1) put_voxel(p, q, kb + kk, j, i, acc[kk], overwrite);
         acc[kk] = 0.f;
         q += plane;
     }
@@ -937,7 +939,7 @@ template <int KC>
 __device__ __forceinline__ void flush_x2_triple(f2x (&acc)[KC / 2], const BPParams& p, int i,
                                                 int j, int kb, bool overwrite)
 {
-    float* q = p.vol + ((long)(kb - p.k0) * p.Ny + j) * p.Nx + i;
+    float* q = vol_voxel(p, kb, j, i);
     long plane = (long)p.Ny * p.Nx;
     asm volatile("mov.b64 %0, %0;" : "+l"(plane));
 #pragma unroll
@@ -951,7 +953,7 @@ __device__ __forceinline__ void flush_x2_triple(f2x (&acc)[KC / 2], const BPPara
             half = (kk - 60) >> 1;
         }
         const float v = half ? hi2(acc[pi]) : lo2(acc[pi]);
-        *q = overwrite ? v : *q + v;
+        put_voxel(p, q, kb + kk, j, i, v, overwrite);
         q += plane;
     }
 #pragma unroll
@@ -1058,6 +1060,535 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
+// ----------------------------------------------------------------------------------------
+// TMEM-accumulator form of the TRIPLE RAW walks (walks 9 / 10 = 6 / 7 with the accumulators in
+// tensor memory).  The register-resident walk holds 64 fp32 accumulators per thread (127
+// registers, 2 CTAs = 16 warps per SM) and its measured limit is latency: 64.5 % issue, the
+// top stall "wait" (fixed-latency dependencies; profiles/r2/ncu_bp_kernel_full_r2b.txt).  Here
+// each thread's 64 partial sums live in TMEM (warp w owns lanes 32 (w % 4) .. +31 and 64
+// columns at 64 (w / 4) of its CTA's 128-column allocation) and a view is walked in three
+// sub-walks of 24 / 24 / 16 slices: tcgen05.ld the sub-walk's accumulators, the same FFMA2
+// arithmetic in registers, tcgen05.st them back.  Freed registers buy a third CTA per SM
+// (24 warps, 80 registers).  TMEM traffic is 8 B per update (4 B read, 4 B written) against a
+// 64 B/clk per SM read port (B300_MICROARCH.md: TMEM), i.e. <= 55 % of it at 2,500 GUPS.  The
+// order of every floating-point operation is the register walk's, so the result is bitwise
+// that of walks 6 / 7 (and their partial-chunk companions 3 / 8).
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, f2x (&a)[8])
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+#pragma unroll
+    for (int m = 0; m < 8; ++m) a[m] = pk2(__uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, f2x (&a)[4])
+{
+    uint32_t r[8];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7])
+        : "r"(taddr));
+#pragma unroll
+    for (int m = 0; m < 4; ++m) a[m] = pk2(__uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
+}
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const f2x (&a)[8])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+        "f"(lo2(a[0])), "f"(hi2(a[0])), "f"(lo2(a[1])), "f"(hi2(a[1])), "f"(lo2(a[2])),
+        "f"(hi2(a[2])), "f"(lo2(a[3])), "f"(hi2(a[3])), "f"(lo2(a[4])), "f"(hi2(a[4])),
+        "f"(lo2(a[5])), "f"(hi2(a[5])), "f"(lo2(a[6])), "f"(hi2(a[6])), "f"(lo2(a[7])),
+        "f"(hi2(a[7])));
+}
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const f2x (&a)[4])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+        "f"(lo2(a[0])), "f"(hi2(a[0])), "f"(lo2(a[1])), "f"(hi2(a[1])), "f"(lo2(a[2])),
+        "f"(hi2(a[2])), "f"(lo2(a[3])), "f"(hi2(a[3])));
+}
+__device__ __forceinline__ void tm_ld4(uint32_t taddr, f2x (&a)[2])
+{
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+    a[0] = pk2(__uint_as_float(r[0]), __uint_as_float(r[1]));
+    a[1] = pk2(__uint_as_float(r[2]), __uint_as_float(r[3]));
+}
+__device__ __forceinline__ void tm_st4(uint32_t taddr, const f2x (&a)[2])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+                 "f"(lo2(a[0])), "f"(hi2(a[0])), "f"(lo2(a[1])), "f"(hi2(a[1])));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// (c >= 0 ? a : b) per fp32x2 half (PTX slct: one FSEL per half instead of two predicated moves)
+__device__ __forceinline__ float slct(float a, float b, float c)
+{
+    float d;
+    asm("slct.f32.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+__device__ __forceinline__ f2x sel2(f2x a, f2x b, f2x c)
+{
+    return pk2(slct(lo2(a), lo2(b), lo2(c)), slct(hi2(a), hi2(b), hi2(c)));
+}
+
+// Triple groups q = Q0 .. Q0+NQ-1 of accumulate_view_raw_x2_triple (and its closing PAIR quad
+// when QUAD) on the accumulator pairs acc[3 (q - Q0) + r] (the quad: acc[3 NQ], acc[3 NQ + 1]).
+// Same operations in the same order, so bitwise the same sums.
+template <int BW, bool ROWS3, int Q0, int NQ, bool QUAD>
+__device__ __forceinline__ void triple_groups(f2x (&acc)[3 * NQ + (QUAD ? 2 : 0)], uint32_t a0,
+                                              const ThreadInv& t)
+{
+    constexpr uint32_t S = BW * 4;
+    const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
+    const f2x du2 = pk2(t.du, t.du);
+    const f2x magic2 = pk2(8388608.0f, 8388608.0f), nmagic2 = pk2(-8388608.0f, -8388608.0f);
+    const f2x fv02 = pk2(t.fv0, t.fv0);
+    // (kk, kk + 3) in a register stepped by FADD2 (exact small integers): one instruction per
+    // group instead of two uniform moves of the constants
+    f2x kvec = pk2((float)(6 * Q0), (float)(6 * Q0 + 3));
+    asm volatile("mov.b64 %0, %0;" : "+l"(kvec));
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+        const f2x v = fma2(kvec, dv2, fv02);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(kvec) : "l"(pk2(6.f, 6.f)));
+        const f2x tb = add2_rd(v, magic2);
+        const f2x fr = sub2(v, add2(tb, nmagic2));
+        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        constexpr int NR = ROWS3 ? 3 : 4;
+        f2x h[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const f2x a = pk2(lds32(adA + r * S), lds32(adB + r * S));
+            const f2x b = pk2(lds32(adA + r * S + 4), lds32(adB + r * S + 4));
+            h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
+        }
+        const f2x d01 = sub2(h[1], h[0]), d12 = sub2(h[2], h[1]);
+        const f2x g1 = add2(fr, dvm12);
+        const f2x e1 = sel2(d12, d01, g1);
+        acc[3 * qq] = fma2(W2, fma2(fr, d01, h[0]), acc[3 * qq]);  // line 6; Alg. alg:bp line 10
+        acc[3 * qq + 1] = fma2(W2, fma2(g1, e1, h[1]), acc[3 * qq + 1]);
+        if constexpr (ROWS3) {
+            const f2x g2 = add2(g1, dv2);
+            acc[3 * qq + 2] = fma2(W2, fma2(g2, sel2(d12, d01, g2), h[1]), acc[3 * qq + 2]);
+        } else {
+            const f2x d23 = sub2(h[NR - 1], h[2]);
+            const f2x g2 = add2(g1, dvm12);
+            acc[3 * qq + 2] = fma2(W2, fma2(g2, sel2(d23, d12, g2), h[2]), acc[3 * qq + 2]);
+        }
+    }
+    if constexpr (QUAD) {  // slices 60..63
+        const f2x v = fma2(pk2(60.f, 62.f), dv2, fv02);
+        const f2x tb = add2_rd(v, magic2);
+        const f2x fr = sub2(v, add2(tb, nmagic2));
+        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        f2x h[3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const f2x a = pk2(lds32(adA + r * S), lds32(adB + r * S));
+            const f2x b = pk2(lds32(adA + r * S + 4), lds32(adB + r * S + 4));
+            h[r] = fma2(du2, sub2(b, a), a);
+        }
+        const f2x d01 = sub2(h[1], h[0]), d12 = sub2(h[2], h[1]);
+        const f2x g = add2(fr, dvm12);
+        acc[3 * NQ] = fma2(W2, fma2(fr, d01, h[0]), acc[3 * NQ]);
+        acc[3 * NQ + 1] = fma2(W2, fma2(g, sel2(d12, d01, g), h[1]), acc[3 * NQ + 1]);
+    }
+}
+
+// The 64 accumulators of one thread: pair m = columns 2m, 2m + 1.  SUB = 4: sub-walks of four
+// groups (pairs 0..11, 12..23) and the rest (24..31); SUB = 2: five sub-walks of two groups
+// (pairs 0..5, .., 18..23) and the rest (24..31) -- fewer live accumulators, for 4 CTAs / SM.
+template <int BW, bool ROWS3, int Q0, int NQ>
+__device__ __forceinline__ void tmem_sub(uint32_t tacc, uint32_t a0, const ThreadInv& t)
+{
+    constexpr int NP = 3 * NQ;  // 12 or 6 pairs = 24 or 12 columns
+    f2x acc[NP];
+    if constexpr (NP == 12) {
+        f2x x[8], y[4];
+        tm_ld16(tacc + 6 * Q0, x);
+        tm_ld8(tacc + 6 * Q0 + 16, y);
+        tm_wait_ld();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[m] = x[m];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[8 + m] = y[m];
+    } else {
+        f2x x[4], y[2];
+        tm_ld8(tacc + 6 * Q0, x);
+        tm_ld4(tacc + 6 * Q0 + 8, y);
+        tm_wait_ld();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[m] = x[m];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) acc[4 + m] = y[m];
+    }
+    triple_groups<BW, ROWS3, Q0, NQ, false>(acc, a0, t);
+    if constexpr (NP == 12) {
+        f2x x[8], y[4];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[m] = acc[m];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) y[m] = acc[8 + m];
+        tm_st16(tacc + 6 * Q0, x);
+        tm_st8(tacc + 6 * Q0 + 16, y);
+    } else {
+        f2x x[4], y[2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) x[m] = acc[m];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) y[m] = acc[4 + m];
+        tm_st8(tacc + 6 * Q0, x);
+        tm_st4(tacc + 6 * Q0 + 8, y);
+    }
+}
+
+template <int BW, bool ROWS3, int SUB>
+__device__ __forceinline__ void walk_view_tmem(uint32_t tacc, uint32_t a0, const ThreadInv& t)
+{
+    tm_wait_st();  // the previous view's stores of these columns
+    if constexpr (SUB == 4) {
+        tmem_sub<BW, ROWS3, 0, 4>(tacc, a0, t);
+        tmem_sub<BW, ROWS3, 4, 4>(tacc, a0, t);
+    } else {
+        tmem_sub<BW, ROWS3, 0, 2>(tacc, a0, t);
+        tmem_sub<BW, ROWS3, 2, 2>(tacc, a0, t);
+        tmem_sub<BW, ROWS3, 4, 2>(tacc, a0, t);
+        tmem_sub<BW, ROWS3, 6, 2>(tacc, a0, t);
+    }
+    {
+        f2x acc[8];
+        tm_ld16(tacc + 48, acc);
+        tm_wait_ld();
+        triple_groups<BW, ROWS3, 8, 2, true>(acc, a0, t);
+        tm_st16(tacc + 48, acc);
+    }
+}
+
+// Flush: every slice's partial sum to the volume (mapping of flush_x2_triple), zeros back.
+template <int KC>
+__device__ __forceinline__ void flush_tmem_triple(uint32_t tacc, const BPParams& p, int i, int j,
+                                                  int kb, bool overwrite, bool inside)
+{
+    tm_wait_st();
+    float* q0 = vol_voxel(p, kb, j, i);
+    const long plane = (long)p.Ny * p.Nx;
+    const f2x zero[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int part = 0; part < 4; ++part) {  // pairs 8 part .. 8 part + 7
+        f2x a[8];
+        tm_ld16(tacc + 16 * part, a);
+        tm_wait_ld();
+        if (inside) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int pi = 8 * part + m;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int kk = pi < 30 ? 6 * (pi / 3) + 3 * half + pi % 3
+                                           : 60 + 2 * half + (pi - 30);
+                    const float v = half ? hi2(a[m]) : lo2(a[m]);
+                    put_voxel(p, q0 + kk * plane, kb + kk, j, i, v, overwrite);
+                }
+            }
+        }
+        tm_st16(tacc + 16 * part, zero);
+    }
+}
+
+// TRI 1: 4-row TRIPLE (walk 9), 2: 3-row TRIPLE (walk 10).  Three CTAs per SM (80 registers,
+// 3 x 128 TMEM columns).  Measured alternatives (B200, config 4 / config 5 slab, 256 views):
+// four CTAs per SM with 12-slice sub-walks (64 registers) 2078 / 2304 GUPS vs 2089 / 2311;
+// no CTA barrier per view (the last warp out of a buffer refills it) 1908 / 2062 -- warps drift
+// apart and the refill lands late (28.7 % long-scoreboard stalls on the box barrier).
+template <int BW, int TRI, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    bp_tmem_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
+                   const __grid_constant__ PTable pt)
+{
+    constexpr int KC = 64;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
+    const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
+    if (tile_i >= p.tiles_i) return;
+    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    const int ic = min(i, p.Nx - 1), jc = min(j, p.Ny - 1);
+    const int i_corner = (lane & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
+    const int j_corner = (lane & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
+    const int kb = p.kb0 + (int)blockIdx.y * KC;
+    if (kb < p.k0 || kb + KC > p.k0 + p.nk) __trap();  // whole chunks only (host)
+    const int n = (int)p.n_views;
+
+    unsigned char* const raw = smem;
+    Meta* const meta = reinterpret_cast<Meta*>(raw + kRawBuf * p.raw_bytes);
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
+    uint32_t* const tslot = reinterpret_cast<uint32_t*>(mbar + kRawBuf);
+    const uint32_t tx_bytes = (uint32_t)(BW * p.box_h * 4);
+    const CUtensorMap* const tmap_ptr = &tmap;
+    const PTable* const ptab = &pt;
+    const uint32_t raw0 = smem_u32(raw);
+
+    auto issue = [=](int t) {
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        if (!m.fast) __trap();
+        const int b = t % kRawBuf;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[b], tx_bytes);
+        tma_load_3d(raw + b * p.raw_bytes, tmap_ptr, &mbar[b], m.u_org, m.v_org - p.v0, t);
+    };
+    auto metas = [=](int t0) {
+        if (t0 + warp < n)
+            compute_meta1<KC, 2>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner, kb,
+                                 0, KC);
+    };
+
+    if (warp == 0) {  // 128 TMEM columns: 64 per warp pair (w, w + 4) sharing a lane quarter
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                         smem_u32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int b = 0; b < kRawBuf; ++b) mbar_init(&mbar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    metas(0);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tacc = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    if (tid == 0)
+        for (int t = 0; t < kRawBuf && t < n; ++t) issue(t);
+    {
+        const f2x zero[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int part = 0; part < 4; ++part) tm_st16(tacc + 16 * part, zero);
+    }
+
+    // the host always sums in 128-view batches (p.vb): a power of two here, so the flush test is
+    // a mask, not a division
+    constexpr int VB = 128;
+    if (p.vb != VB) __trap();
+    const int first_flush = (int)(VB - 1 - (p.s0 % VB + VB) % VB);
+    // the column's coordinates as doubles, hoisted (80 registers leave room for them)
+    const double di = ic, dj = jc, dk = kb;
+    for (int t = 0; t < n; ++t) {
+        const ThreadInv ti = split(column_invariants(ptab->P[t], di, dj, dk));
+        const int b = t % kRawBuf;
+        mbar_wait(&mbar[b], (uint32_t)((t / kRawBuf) & 1));
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        const int u_org = m.u_org, v_org = m.v_org;
+        const uint32_t rb = raw0 + (uint32_t)(b * p.raw_bytes);
+        const uint32_t a0 =
+            rb + (uint32_t)(((ti.nv - v_org) * BW + (ti.nu - u_org)) * 4) + p.neg_magic;
+        walk_view_tmem<BW, TRI == 2, MINB == 3 ? 4 : 2>(tacc, a0, ti);
+        if ((t >= first_flush && ((t - first_flush) & (VB - 1)) == 0) || t == n - 1) {
+            const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+            const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+            const bool ow = !p.accumulate && t <= first_flush;
+            flush_tmem_triple<KC>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
+        }
+        if (((t + kRawBuf + 1) & 7) == 0) metas(t + kRawBuf + 1);
+        __syncthreads();  // buffer b read out by every warp
+        if (tid == 0 && t + kRawBuf < n) issue(t + kRawBuf);
+    }
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tslot)
+                     : "memory");
+}
+
+// Two views per step (walks 11 / 12 = 9 / 10 stepping two views at a time): every sub-walk
+// loads its accumulators from TMEM once, adds view t's and then view t + 1's updates (the same
+// per-voxel order, so bitwise the same sums) and stores them once.  The two views' tap loads and
+// interpolations are independent, which doubles the work the scheduler can interleave, and the
+// per-step costs (TMEM traffic, box barrier, CTA barrier, TMA issue) are shared by two views.
+// (A one-view step -- view 0 when the first flush falls on it, or the last view -- walks the
+// view a second time with weight 0, which adds +0 to each sum.)  Six boxes in flight (two steps
+// of prefetch).  A step ends on every flush point of the two-level sum.
+// Measured (B200, 256 views; config 4 / config 5 slab): 2220 / 2480 GUPS vs 2133 / 2345 for
+// one view per step (walks 9 / 10); a generic V-view form was slower (V = 2: 2161 / 2378,
+// V = 3: 2168 / 2407) -- its per-view padding and buffer bookkeeping cost more than V = 3 saves.
+constexpr int kRawBuf2 = 6;
+
+template <int BW, bool ROWS3, int Q0, int NQ>
+__device__ __forceinline__ void tmem_sub2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
+                                          uint32_t a1, const ThreadInv& u)
+{
+    constexpr int NP = 3 * NQ;  // 6 pairs = 12 columns
+    static_assert(NP == 6, "two-group sub-walks");
+    f2x acc[NP];
+    {
+        f2x x[4], y[2];
+        tm_ld8(tacc + 6 * Q0, x);
+        tm_ld4(tacc + 6 * Q0 + 8, y);
+        tm_wait_ld();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) acc[m] = x[m];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) acc[4 + m] = y[m];
+    }
+    triple_groups<BW, ROWS3, Q0, NQ, false>(acc, a0, t);
+    triple_groups<BW, ROWS3, Q0, NQ, false>(acc, a1, u);
+    {
+        f2x x[4], y[2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) x[m] = acc[m];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) y[m] = acc[4 + m];
+        tm_st8(tacc + 6 * Q0, x);
+        tm_st4(tacc + 6 * Q0 + 8, y);
+    }
+}
+
+template <int BW, bool ROWS3>
+__device__ __forceinline__ void walk_views_tmem2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
+                                                 uint32_t a1, const ThreadInv& u)
+{
+    tm_wait_st();
+    tmem_sub2<BW, ROWS3, 0, 2>(tacc, a0, t, a1, u);
+    tmem_sub2<BW, ROWS3, 2, 2>(tacc, a0, t, a1, u);
+    tmem_sub2<BW, ROWS3, 4, 2>(tacc, a0, t, a1, u);
+    tmem_sub2<BW, ROWS3, 6, 2>(tacc, a0, t, a1, u);
+    {
+        f2x acc[8];
+        tm_ld16(tacc + 48, acc);
+        tm_wait_ld();
+        triple_groups<BW, ROWS3, 8, 2, true>(acc, a0, t);
+        triple_groups<BW, ROWS3, 8, 2, true>(acc, a1, u);
+        tm_st16(tacc + 48, acc);
+    }
+}
+
+template <int BW, int TRI>
+__global__ void __launch_bounds__(kThreads, 3)
+    bp_tmem2_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
+                    const __grid_constant__ PTable pt)
+{
+    constexpr int KC = 64, NB = kRawBuf2, VB = 128;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
+    const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
+    if (tile_i >= p.tiles_i) return;
+    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    const int ic = min(i, p.Nx - 1), jc = min(j, p.Ny - 1);
+    const int i_corner = (lane & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
+    const int j_corner = (lane & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
+    const int kb = p.kb0 + (int)blockIdx.y * KC;
+    if (kb < p.k0 || kb + KC > p.k0 + p.nk) __trap();  // whole chunks only (host)
+    if (p.vb != VB) __trap();
+    const int n = (int)p.n_views;
+
+    unsigned char* const raw = smem;
+    Meta* const meta = reinterpret_cast<Meta*>(raw + NB * p.raw_bytes);
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
+    uint32_t* const tslot = reinterpret_cast<uint32_t*>(mbar + NB);
+    const uint32_t tx_bytes = (uint32_t)(BW * p.box_h * 4);
+    const CUtensorMap* const tmap_ptr = &tmap;
+    const PTable* const ptab = &pt;
+    const uint32_t raw0 = smem_u32(raw);
+
+    auto issue = [=](int t) {
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        if (!m.fast) __trap();
+        const int b = t % NB;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[b], tx_bytes);
+        tma_load_3d(raw + b * p.raw_bytes, tmap_ptr, &mbar[b], m.u_org, m.v_org - p.v0, t);
+    };
+    auto metas = [=](int t0) {
+        if (t0 + warp < n)
+            compute_meta1<KC, 2>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner, kb,
+                                 0, KC);
+    };
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                         smem_u32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    metas(0);
+    int meta_next = 8;  // views with boxes computed: 0 .. meta_next - 1
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tacc = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    if (tid == 0)
+        for (int t = 0; t < NB && t < n; ++t) issue(t);
+    {
+        const f2x zero[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int part = 0; part < 4; ++part) tm_st16(tacc + 16 * part, zero);
+    }
+
+    const int first_flush = (int)(VB - 1 - (p.s0 % VB + VB) % VB);
+    const double di = ic, dj = jc, dk = kb;
+    const uint32_t nm = p.neg_magic;
+    for (int t = 0; t < n;) {
+        const bool two = t + 1 < n && !(t == 0 && (first_flush & 1) == 0);
+        const int te = two ? t + 1 : t;
+        const ThreadInv ti = split(column_invariants(ptab->P[t], di, dj, dk));
+        ThreadInv tu = split(column_invariants(ptab->P[te], di, dj, dk));
+        if (!two) tu.W = 0.f;
+        mbar_wait(&mbar[t % NB], (uint32_t)((t / NB) & 1));
+        if (two) mbar_wait(&mbar[te % NB], (uint32_t)((te / NB) & 1));
+        const Meta& m0 = meta[t & (kMetaRing - 1)];
+        const Meta& m1 = meta[te & (kMetaRing - 1)];
+        const uint32_t a0 = raw0 + (uint32_t)((t % NB) * p.raw_bytes) +
+                            (uint32_t)(((ti.nv - m0.v_org) * BW + (ti.nu - m0.u_org)) * 4) + nm;
+        const uint32_t a1 = raw0 + (uint32_t)((te % NB) * p.raw_bytes) +
+                            (uint32_t)(((tu.nv - m1.v_org) * BW + (tu.nu - m1.u_org)) * 4) + nm;
+        walk_views_tmem2<BW, TRI == 2>(tacc, a0, ti, a1, tu);
+        if ((te >= first_flush && ((te - first_flush) & (VB - 1)) == 0) || te == n - 1) {
+            const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+            const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+            const bool ow = !p.accumulate && te <= first_flush;
+            flush_tmem_triple<KC>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
+        }
+        if (te + NB >= meta_next && meta_next < n) {  // boxes of the next eight views
+            metas(meta_next);
+            meta_next += 8;
+        }
+        __syncthreads();  // the step's buffers read out by every warp; new boxes written
+        if (tid == 0)
+            for (int v = t + NB; v <= te + NB; ++v)
+                if (v < n) issue(v);
+        t = te + 1;
+    }
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tslot)
+                     : "memory");
+}
+
 // Opt-in dynamic shared memory per CTA of the current device.
 int max_dyn_smem()
 {
@@ -1116,22 +1647,24 @@ bool use_pair(const ifdk_geometry* g)
 std::atomic<int> g_walk_override{0}, g_raster_override{0};
 
 // Slices per floor of the k-walk.  Default where dv/dk < 1 for every z (all five configs):
-// the TRIPLE RAW walks -- 4-row (6) where 0.5 <= dv/dk (configs 1-4: 2000 vs 1884 GUPS for
-// the PAIR RAW walk on config 4), 3-row (7) where dv/dk < 0.5 everywhere (config 5) -- and
-// the PAIR RAW walk (5) in between; their partial chunks run on the pair-patch companions
+// the TRIPLE walks with TMEM accumulators, two views per step -- 4-row (11) where
+// 0.5 <= dv/dk (configs 1-4), 3-row (12) where dv/dk < 0.5 everywhere (config 5); measured on
+// config 4 / the config-5 slab (256 views): 2220 / 2480 GUPS vs 2133 / 2345 for one view per
+// step (9 / 10) and 2022 / 2197 for the register walks (6 / 7; 2000 vs 1884 for PAIR RAW 5) --
+// and the PAIR RAW walk (5) in between; their partial chunks run on the pair-patch companions
 // 3, 8 and 4, bitwise equal.  dv/dk >= 1 somewhere: one floor per slice (walk 1, 32-slice
 // chunks).  The override (ifdk_set_bp_variant) picks among the bitwise-equal walks of the
-// geometry's family: 2, 4, 5 (PAIR), 3, 6 (4-row TRIPLE), 7, 8 (3-row TRIPLE).
+// geometry's family: 2, 4, 5 (PAIR), 3, 6, 9, 11 (4-row TRIPLE), 7, 8, 10, 12 (3-row TRIPLE).
 int choose_walk(const ifdk_geometry* g)
 {
     if (!use_pair(g)) return 1;
     const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
     const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
-    int w = dv_min >= 0.5001 ? 6 : dv_max < 0.4999 ? 7 : 5;
+    int w = dv_min >= 0.5001 ? 11 : dv_max < 0.4999 ? 12 : 5;
     const int v = g_walk_override.load(std::memory_order_relaxed);
     if (v == 2 || v == 4 || v == 5) w = v;
-    if ((v == 3 || v == 6) && dv_min >= 0.5001) w = v;
-    if ((v == 7 || v == 8) && dv_max < 0.4999) w = v;
+    if ((v == 3 || v == 6 || v == 9 || v == 11) && dv_min >= 0.5001) w = v;
+    if ((v == 7 || v == 8 || v == 10 || v == 12) && dv_max < 0.4999) w = v;
     return w;
 }
 
@@ -1147,7 +1680,8 @@ namespace {
 
 // One launch over views s0 .. s0+n_views-1 (n_views <= kMaxViewsPerLaunch).
 ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n_views, int v0,
-                         int n_rows, float* vol, int k0, int nk, int accumulate, cudaStream_t st)
+                         int n_rows, float* vol, int k0, int nk, int accumulate, cudaStream_t st,
+                         const RedDest* red)
 {
     // Per-view projection matrices (fp64), passed in the kernel's parameter space.
     PTable pt;
@@ -1168,6 +1702,14 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     const int n_chunks = (k0 + nk - p.kb0 + KC - 1) / KC;
     p.vb = 128;
     p.accumulate = accumulate;
+    if (red) {
+        p.red = red->mode + 1;
+        p.n_dest = red->n;
+        for (int d = 0; d < red->n; ++d) {
+            p.dest_k0[d] = red->k0[d];
+            p.dest[d] = red->base[d];
+        }
+    }
 
     // Box of the staged patch from the conservative geometric bound.
     double wb, hb;
@@ -1194,7 +1736,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         int box_w = box_w0, P2 = 0, BW = 0;
         for (int c : {24, 40, 56, 72})
             if (c >= box_w - 1) { P2 = c; break; }
-        if (w == 5 || w == 6 || w == 7) {
+        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 12)) {
             for (int c : {40, 72})  // row pitch = 8 mod 32 words: conflict-free LDS.32 taps
                 if (c >= box_w) { BW = c; break; }
             box_w = BW;
@@ -1207,7 +1749,14 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             q.box_w = box_w;
             q.box_h = box_h;
             q.raw_bytes = (box_w * box_h * 4 + 127) / 128 * 128;
-            smem = BW ? kRawBuf * (size_t)q.raw_bytes + kMetaRing * sizeof(Meta) + 8 * kRawBuf
+            auto raw_smem = [&](int nbuf) {
+                return nbuf * (size_t)q.raw_bytes + kMetaRing * sizeof(Meta) + 8 * nbuf + 16;
+            };
+            // two views per step want six boxes; where those do not fit three CTAs per SM
+            // (tall or wide boxes) the one-view step (four boxes) is the faster choice
+            if ((w == 11 || w == 12) && 3 * (raw_smem(kRawBuf2) + 1024) > 228 * 1024) w -= 2;
+            const int nbuf = (w == 11 || w == 12) ? kRawBuf2 : kRawBuf;
+            smem = BW ? raw_smem(nbuf)
                       : 2 * (size_t)q.raw_bytes + 2 * sizeof(float2) * box_h * P2 +
                             kMetaRing * sizeof(Meta) + 16;
             cuuint64_t dims[3] = {(cuuint64_t)g->Nu, (cuuint64_t)n_rows, (cuuint64_t)n_views};
@@ -1232,6 +1781,20 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         q.neg_magic = 0u - 0x4B000000u * (uint32_t)(BW ? BW * 4 : P2 * 8);
         dim3 grid((unsigned)(q.raster * tiles_j), (unsigned)nch,
                   (unsigned)((q.tiles_i + q.raster - 1) / q.raster));
+        if (BW && w >= 9 && w <= 12) {
+            auto k = w == 9    ? (BW == 40 ? bp_tmem_kernel<40, 1, 3> : bp_tmem_kernel<72, 1, 3>)
+                     : w == 10 ? (BW == 40 ? bp_tmem_kernel<40, 2, 3> : bp_tmem_kernel<72, 2, 3>)
+                     : w == 11 ? (BW == 40 ? bp_tmem2_kernel<40, 1> : bp_tmem2_kernel<72, 1>)
+                               : (BW == 40 ? bp_tmem2_kernel<40, 2> : bp_tmem2_kernel<72, 2>);
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp tmem)");
+            k<<<grid, kThreads, smem, st>>>(q, map, pt);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "bp_tmem_kernel launch");
+            count_launch();
+            return IFDK_OK;
+        }
         if (BW) {
             auto k = w == 6   ? (BW == 40 ? bp_raw_kernel<64, 40, 1> : bp_raw_kernel<64, 72, 1>)
                      : w == 7 ? (BW == 40 ? bp_raw_kernel<64, 40, 2> : bp_raw_kernel<64, 72, 2>)
@@ -1246,8 +1809,8 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             return IFDK_OK;
         }
         if (w == 5) w = 4;
-        if (w == 6) w = 3;
-        if (w == 7) w = 8;
+        if (w == 6 || w == 9 || w == 11) w = 3;
+        if (w == 7 || w == 10 || w == 12) w = 8;
         if (w == 8) {
             switch (P2) {
                 case 24: return launch_t<64, 24, 8>(q, map, pt, tma, grid, smem, st);
@@ -1293,7 +1856,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         }
     };
 
-    if ((walk != 5 && walk != 6 && walk != 7) || !tma_ok || box_w0 > 72)
+    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 12)) || !tma_ok || box_w0 > 72)
         return run(walk, p.kb0, n_chunks);
     // RAW staging runs the whole chunks; a partial chunk at either slab end (its masked slices
     // would read rows outside the box) takes the x2 pair walk, bitwise the same values.
@@ -1302,7 +1865,8 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     ifdk_status s = IFDK_OK;
     if (c1 > c0) s = run(walk, p.kb0 + c0 * KC, c1 - c0);
     // partial chunks: walk 4 for walk 5, 3 for 6, 8 for 7 (bitwise the same arithmetic)
-    const int wp = walk == 6 ? 3 : walk == 7 ? 8 : 4;
+    const int wp = (walk == 6 || walk == 9 || walk == 11) ? 3
+                   : (walk == 7 || walk == 10 || walk == 12) ? 8 : 4;
     if (s == IFDK_OK && head) s = run(wp, p.kb0, 1);
     if (s == IFDK_OK && tail && (n_chunks - 1 > 0 || !head)) s = run(wp, p.kb0 + (n_chunks - 1) * KC, 1);
     return s;
@@ -1348,6 +1912,15 @@ void preload_bp_kernels()
     touch_kernel(bp_raw_kernel<64, 72, 1>);
     touch_kernel(bp_raw_kernel<64, 40, 2>);
     touch_kernel(bp_raw_kernel<64, 72, 2>);
+    touch_kernel(bp_tmem_kernel<40, 1, 3>);
+    touch_kernel(bp_tmem_kernel<72, 1, 3>);
+    touch_kernel(bp_tmem_kernel<40, 2, 3>);
+    touch_kernel(bp_tmem_kernel<72, 2, 3>);
+    touch_kernel(bp_tmem2_kernel<40, 1>);
+    touch_kernel(bp_tmem2_kernel<72, 1>);
+    touch_kernel(bp_tmem2_kernel<40, 2>);
+    touch_kernel(bp_tmem2_kernel<72, 2>);
+
 }
 
 void set_bp_variant(int walk, int raster)
@@ -1358,8 +1931,9 @@ void set_bp_variant(int walk, int raster)
 
 ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
-                               cudaStream_t st)
+                               cudaStream_t st, const RedDest* red)
 {
+    if (n_views == 0 && red) return IFDK_OK;  // nothing to add
     if (n_views == 0) {
         if (!accumulate) {
             cudaError_t e =
@@ -1379,7 +1953,7 @@ ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, 
         long n = stop - s;
         if (n > n_views - t) n = n_views - t;
         ifdk_status r = launch_range(g, Q + (size_t)t * view_elems, s, n, v0, n_rows, vol, k0, nk,
-                                     (accumulate || t > 0) ? 1 : 0, st);
+                                     (accumulate || t > 0) ? 1 : 0, st, red);
         if (r != IFDK_OK) return r;
         t += n;
     }

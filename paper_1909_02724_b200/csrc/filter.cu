@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "ifdk_internal.h"
+#include "mbar.cuh"
 
 namespace ifdk {
 namespace {
@@ -156,10 +157,10 @@ __global__ void __launch_bounds__(kThreads) filter_fft_kernel(const FilterParams
             if (m < p.Nu) {
                 const float uh = ((float)m - p.cu) * p.Du;
                 const float uh2 = uh * uh;
-                const float wA = p.D / sqrtf(p.D2 + uh2 + vhA * vhA);
+                const float wA = 1.0f / sqrtf(p.D2 + uh2 + vhA * vhA);  // D is in H
                 x.x = __ldg(eA + m) * wA;
                 if (hasB) {
-                    const float wB = p.D / sqrtf(p.D2 + uh2 + vhB * vhB);
+                    const float wB = 1.0f / sqrtf(p.D2 + uh2 + vhB * vhB);
                     x.y = __ldg(eB + m) * wB;
                 }
             }
@@ -260,11 +261,27 @@ __device__ __forceinline__ cx cfma2(cx a, cx b, cx c)  // element-wise a b + c
 }
 __device__ __forceinline__ cx negi(cx v) { return mk(im_(v), -re_(v)); }  // -i v
 
-// a b = a.re (b.re, b.im) + a.im (-b.im, b.re)
+// a b = b.re (a.re, a.im) + b.im (-a.im, a.re): the swapped, half-negated operand i a sits in
+// the first source slot, where ptxas folds it into a .LO_HI.NP operand modifier, and b's halves
+// are register broadcasts -- one FMUL2 + one FFMA2, no moves (the form with i b in the second
+// slot cost a MOV and an FADD per product).
+__device__ __forceinline__ cx ia(cx v) { return mk(-im_(v), re_(v)); }  // i v
 __device__ __forceinline__ cx cmulf(cx a, cx b)
 {
-    const float ar = re_(a), ai = im_(a);
-    return cfma2(mk(ai, ai), mk(-im_(b), re_(b)), cmul2(mk(ar, ar), b));
+    const float br = re_(b), bi = im_(b);
+    return cfma2(ia(a), mk(bi, bi), cmul2(a, mk(br, br)));
+}
+__device__ __forceinline__ float rsqrt_ftz(float x)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// a (c + i s) for compile-time c, s: FMUL2 / FFMA2 with broadcast immediates
+__device__ __forceinline__ cx cmulk(cx a, float c, float s)
+{
+    return cfma2(ia(a), mk(s, s), cmul2(a, mk(c, c)));
 }
 
 __device__ __forceinline__ void dft4(cx& a, cx& b, cx& c, cx& d)
@@ -278,23 +295,41 @@ __device__ __forceinline__ void dft4(cx& a, cx& b, cx& c, cx& d)
     d = csub(t1, t3);
 }
 
+// dft4 of (a, b, 0, 0): the zero-padded upper half of a row costs no additions
+__device__ __forceinline__ void dft4_half(cx& a, cx& b, cx& c, cx& d)
+{
+    const cx t3 = negi(b);  // -i b
+    c = csub(a, b);
+    d = csub(a, t3);
+    const cx a0 = a;
+    a = cadd(a0, b);
+    b = cadd(a0, t3);
+}
+
 // 16-point forward DFT in place: n = 4 n1 + n2, k = k1 + 4 k2 (two radix-4 stages).
+// HALF: u[8..15] are zero (the first pass of a zero-padded row).
+template <bool HALF = false>
 __device__ __forceinline__ void dft16(cx (&u)[16])
 {
     constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508977f,
                     C2 = 0.70710678118654752f;
 #pragma unroll
-    for (int n2 = 0; n2 < 4; ++n2) dft4(u[n2], u[4 + n2], u[8 + n2], u[12 + n2]);
+    for (int n2 = 0; n2 < 4; ++n2) {
+        if (HALF)
+            dft4_half(u[n2], u[4 + n2], u[8 + n2], u[12 + n2]);
+        else
+            dft4(u[n2], u[4 + n2], u[8 + n2], u[12 + n2]);
+    }
     // A[n2][k1] (at u[4 k1 + n2]) *= W16^(n2 k1)
-    u[5] = cmulf(u[5], mk(C1, -S1));    // W^1
-    u[6] = cmulf(u[6], mk(C2, -C2));    // W^2
-    u[7] = cmulf(u[7], mk(S1, -C1));    // W^3
-    u[9] = cmulf(u[9], mk(C2, -C2));    // W^2
-    u[10] = negi(u[10]);                // W^4 = -i
-    u[11] = cmulf(u[11], mk(-C2, -C2)); // W^6
-    u[13] = cmulf(u[13], mk(S1, -C1));  // W^3
-    u[14] = cmulf(u[14], mk(-C2, -C2)); // W^6
-    u[15] = cmulf(u[15], mk(-C1, S1));  // W^9
+    u[5] = cmulk(u[5], C1, -S1);    // W^1
+    u[6] = cmulk(u[6], C2, -C2);    // W^2
+    u[7] = cmulk(u[7], S1, -C1);    // W^3
+    u[9] = cmulk(u[9], C2, -C2);    // W^2
+    u[10] = negi(u[10]);            // W^4 = -i
+    u[11] = cmulk(u[11], -C2, -C2); // W^6
+    u[13] = cmulk(u[13], S1, -C1);  // W^3
+    u[14] = cmulk(u[14], -C2, -C2); // W^6
+    u[15] = cmulk(u[15], -C1, S1);  // W^9
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) dft4(u[4 * k1], u[4 * k1 + 1], u[4 * k1 + 2], u[4 * k1 + 3]);
     // X[k1 + 4 k2] sits at u[4 k1 + k2]: transpose by renaming
@@ -332,7 +367,7 @@ __device__ __forceinline__ void twiddle_powers(cx (&w)[16], const cx* tw, int st
 
 // One Stockham radix-16 pass of span P on the values u (= x[i + 256 j]) of thread i; writes
 // the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
-template <int P>
+template <int P, bool HALF = false>
 __device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* tw, int i)
 {
     static_assert(P == 1 || P == 16, "span-1 and span-16 passes");
@@ -343,7 +378,7 @@ __device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* tw, int
 #pragma unroll
         for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
     }
-    dft16(u);
+    dft16<HALF && P == 1>(u);
     const int base = (i - k) * 16 + k;
 #pragma unroll
     for (int m = 0; m < 16; ++m) buf[padx(base + m * P)] = u[m];
@@ -358,9 +393,10 @@ __device__ __forceinline__ void load_in(cx (&u)[16], const cx* buf, int i)
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
 // X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
 // barrier: a buffer is rewritten only after the barrier that follows its last read.
+template <bool HALF = false>  // HALF: x[i + 256 j] = 0 for j >= 8 (a zero-padded 2048-sample row)
 __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const cx* tw, int i)
 {
-    pass_out<1>(u, buf0, tw, i);
+    pass_out<1, HALF>(u, buf0, tw, i);
     __syncthreads();
     load_in(u, buf0, i);
     pass_out<16>(u, buf1, tw, i);
@@ -376,11 +412,12 @@ __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const c
 
 }  // namespace f4k
 
-// ASYNC (rows 16-byte aligned, Nu % 4 == 0): the next row pair is fetched into a shared
-// staging buffer with cp.async while the current pair is transformed, hiding HBM latency.
+// ASYNC (rows 16-byte aligned, Nu % 4 == 0): the next group's rows are fetched into a shared
+// staging buffer by 1-D bulk copies (the TMA engine; one instruction per row, completion on an
+// mbarrier) while the current group is transformed, hiding HBM latency.
 constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
 constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float2) * f4k::kTwEntries +
-                            sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage;
+                            sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage + 16;
 
 // R row pairs per transform (multi-row packing): with N_u <= 2048 / R every row's linear
 // convolution needs only a 2 N_u - 1 window of the length-4096 circular one, so R rows share
@@ -403,27 +440,27 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
     cx* const tw = bufB + (L + L / 16);           // kTwEntries
     float* const Hs = reinterpret_cast<float*>(tw + kTwEntries);  // L/2 + 1 (2052 slots)
     float* const stage = Hs + 2052;                                // ROWS rows of SLOT_F
+    uint64_t* const sbar = reinterpret_cast<uint64_t*>(stage + 2 * kF4kStage);  // staging barrier
     const int i = threadIdx.x;
     for (int e = i; e < kTwEntries; e += T) tw[e] = reinterpret_cast<const cx*>(tw_g)[e];
     for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
     const long n_groups = (p.n_rows_total + ROWS - 1) / ROWS;
-    auto prefetch = [&](long gi) {
-        if (!ASYNC || gi >= n_groups) return;
+    if (ASYNC && i == 0) {
+        mbar_init(sbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto prefetch = [&](long gi) {  // one thread: the group's rows by 1-D bulk copies
+        if (!ASYNC || gi >= n_groups || i != 0) return;
         const long r0 = ROWS * gi;
         const int nrow = (int)min((long)ROWS, p.n_rows_total - r0);
-        const int q4 = p.Nu / 4;
-        for (int c = i; c < nrow * q4; c += T) {
-            const int r = c / q4, cc = c - r * q4;
-            const float* src = p.raw + (r0 + r) * p.Nu + 4 * cc;
-            const uint32_t dst =
-                static_cast<uint32_t>(__cvta_generic_to_shared(stage + r * SLOT_F + 4 * cc));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src)
-                         : "memory");
-        }
-        asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads
+        mbar_expect_tx(sbar, (uint32_t)(nrow * p.Nu * 4));
+        for (int r = 0; r < nrow; ++r)
+            bulk_load(stage + r * SLOT_F, p.raw + (r0 + r) * p.Nu, (uint32_t)(p.Nu * 4), sbar);
     };
     prefetch(blockIdx.x);
-    __syncthreads();
+    uint32_t sphase = 0;
     for (long gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
         const long r0 = ROWS * gi;
         // per slot s: rows A = r0 + 2s (real part), B = r0 + 2s + 1 (imaginary part)
@@ -437,34 +474,42 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             dB[sl] = p.D2 + vhB * vhB;
         }
         if (ASYNC) {
-            asm volatile("cp.async.wait_all;" ::: "memory");
-            __syncthreads();
+            mbar_wait(sbar, sphase);
+            sphase ^= 1u;
         }
         cx u[16];
         // Alg. alg:filter line 2: E~ = E . F_cos (reading c-A5), rows packed per slot, padded.
+        // F_cos = D / sqrt(D^2 + uh^2 + vh^2); D is folded into the filter spectrum H (the
+        // filter is linear), the rows' pair (A, B) shares one FFMA2 and one FMUL2, and the
+        // reciprocal square root is the hardware approximation (<= 2 ulp; the argument is
+        // >= D^2, never denormal) -- far below the filter tolerance.
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
+            if (R == 1 && j >= 8) {  // n = i + 256 j >= 2048 >= N_u: the zero padding
+                u[j] = 0ull;
+                continue;
+            }
             const int sl = j / SJ;
             const int n = i + (j % SJ) * T;
             const long rA = r0 + 2 * sl, rB = rA + 1;
-            float2 x = make_float2(0.f, 0.f);  // (row A, row B)
-            if ((R > 1 || j < 8) && n < p.Nu && rA < p.n_rows_total) {
-                const float uh = ((float)n - p.cu) * p.Du;
-                // F_cos = D / sqrt(D^2 + uh^2 + vh^2); rsqrtf's <= 2 ulp error is far below the
-                // filter tolerance and saves the IEEE sqrt + divide sequences.
-                const float ea = ASYNC ? stage[(2 * sl) * SLOT_F + n] : __ldg(p.raw + rA * p.Nu + n);
-                x.x = ea * (p.D * rsqrtf(fmaf(uh, uh, dA[sl])));
-                if (rB < p.n_rows_total) {
-                    const float eb =
-                        ASYNC ? stage[(2 * sl + 1) * SLOT_F + n] : __ldg(p.raw + rB * p.Nu + n);
-                    x.y = eb * (p.D * rsqrtf(fmaf(uh, uh, dB[sl])));
-                }
+            float ea = 0.f, eb = 0.f;
+            if (ASYNC) {  // read clamped into the row's staging slot; select, no branch
+                const int nc = n < SLOT_F ? n : SLOT_F - 1;  // n >= SLOT_F >= N_u: padding
+                const float sa = stage[(2 * sl) * SLOT_F + nc];
+                const float sb = stage[(2 * sl + 1) * SLOT_F + nc];
+                ea = (n < p.Nu && rA < p.n_rows_total) ? sa : 0.f;
+                eb = (n < p.Nu && rB < p.n_rows_total) ? sb : 0.f;
+            } else if (n < p.Nu && rA < p.n_rows_total) {
+                ea = __ldg(p.raw + rA * p.Nu + n);
+                if (rB < p.n_rows_total) eb = __ldg(p.raw + rB * p.Nu + n);
             }
-            u[j] = mk(x.x, x.y);
+            const float uh = ((float)n - p.cu) * p.Du;
+            const cx q = cfma2(mk(uh, uh), mk(uh, uh), mk(dA[sl], dB[sl]));
+            u[j] = cmul2(mk(ea, eb), mk(rsqrt_ftz(re_(q)), rsqrt_ftz(im_(q))));
         }
         __syncthreads();  // staging read and buffers free: fetch the next group meanwhile
         prefetch(gi + gridDim.x);
-        fft4096(u, buf, bufB, tw, i);
+        fft4096<R == 1>(u, buf, bufB, tw, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -497,7 +542,6 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             }
         }
     }
-    if (ASYNC) asm volatile("cp.async.wait_all;" ::: "memory");
     signal_done(p);
 }
 

@@ -107,7 +107,9 @@ void ensure_filter_tables_host(ifdk_geometry* g)
             const long r = ((long)f * l) % L;
             acc += 2.0 * h[l] * std::cos(2.0 * pi * (double)r / L);
         }
-        g->Hs[f] = (float)(acc * g->C / L);
+        // C / L and the D of F_cos = D / sqrt(D^2 + u^2 + v^2) (the kernels weight by the
+        // reciprocal square root alone; the filter is linear)
+        g->Hs[f] = (float)(acc * g->C * g->D / L);
     }
     g->tw.assign(2 * (size_t)L, 0.f);
     for (int t = 0; t < L; ++t) {

@@ -76,9 +76,20 @@ void preload_filter_kernels();
 void preload_bp_kernels();
 
 // backproject.cu
+// Fused reduce of the projection split (ifdk_backproject_reduce): the flush of each 128-view
+// partial sum adds into the destination slab that holds its slice -- red.global.add (mode 0;
+// local or NVLink-peer memory) or multimem.red (mode 1; multicast mappings).  base[d] holds
+// slices k0[d] .. k0[d + 1] - 1 (the last to the end of the launch's slab), chunk-aligned.
+constexpr int kMaxRedDest = 16;
+struct RedDest {
+    int mode = 0;
+    int n = 0;
+    int k0[kMaxRedDest] = {};
+    float* base[kMaxRedDest] = {};
+};
 ifdk_status launch_backproject(const ifdk_geometry* g, const float* Q, long s0, long n_views,
                                int v0, int n_rows, float* vol, int k0, int nk, int accumulate,
-                               cudaStream_t st);
+                               cudaStream_t st, const RedDest* red = nullptr);
 // tuning hook behind ifdk_set_bp_variant (0 = automatic)
 void set_bp_variant(int walk, int raster);
 

@@ -19,6 +19,12 @@ Two decompositions of the paper's R x C rank grid on one node:
   into a full-size partial volume; a reduce-scatter (sum) of the contiguous
   k-slabs replaces the paper's single MPI_Reduce.  Needs a full
   volume per GPU, so it does not fit config 5.
+* fused projection split (``projection_split_fused``): the same decomposition with the
+  reduce inside the back-projection's write-back -- every 128-view partial sum is added
+  (``ifdk_backproject_reduce``: red.global.add over NVLink, or multimem.red on multicast
+  mappings) straight into the owner's slab, mapped into every rank (``ReduceSlabs``, CUDA
+  IPC).  No partial volume and no reduce-scatter: a rank holds its filtered views and its own
+  slab only, so config 5 fits.
 
 The band exchange is fused into the filter by default: ``PeerExchange`` maps every rank's
 receive buffer into every other rank (CUDA IPC over NVLink), ``ifdk_filter_scatter`` stores
@@ -402,9 +408,12 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
     # the pipeline's streams; the band is then packed and "sent" to itself)
     xchg = world > 1 or (force_exchange and dist.is_available() and dist.is_initialized())
     k0, nk = plan.slab(rank)
-    cuda = vol_slab.is_cuda
+    # vol_slab None: bp_fn writes elsewhere (the fused reduce of hybrid_reconstruct) and is
+    # called with vol None; slices no view touches are then left as they are
+    src = vol_slab if vol_slab is not None else (raw_local if raw_local is not None else raw_host)
+    cuda = src.is_cuda or (vol_slab is None and torch.cuda.is_available() and raw_host is not None)
     S = _Streams(cuda, streams)
-    dev = vol_slab.device
+    dev = src.device if src.is_cuda or vol_slab is not None else torch.device("cuda")
     Nv, Nu = g.Nv, g.Nu
     rounds = plan.n_rounds
     exs = exchanges(g, plan, rank)
@@ -560,11 +569,12 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
                             band, v0 = recvbuf[q][off:off + sz].view(rn, hi - lo + 1, Nu), lo
                         else:  # one rank: back-project straight from the filtered block
                             band, v0 = Qbuf[q][:rn], 0
-                        bp_fn(band, rs0, vol_slab[a - k0:a - k0 + m], a, v0, not acc_first)
+                        bp_fn(band, rs0, None if vol_slab is None else vol_slab[a - k0:a - k0 + m],
+                              a, v0, not acc_first)
                         acc_first = False
                         launched = True
                     off += sz
-                if last and acc_first:  # no view of the whole scan touches these slices
+                if last and acc_first and vol_slab is not None:  # no view touches these slices
                     vol_slab[a - k0:a - k0 + m].zero_()
                 if last and vol_host is not None and m > 0:
                     ev = S.event()
@@ -589,7 +599,7 @@ def _pipeline(g, plan: SlabPlan, rank: int, vol_slab, group, filter_fn, bp_fn, t
             S.record(ev_bp_done[q], S.B)
     if peer is not None:
         peer.rounds_done += rounds
-    if rounds == 0 and nk > 0:  # no views at all
+    if rounds == 0 and nk > 0 and vol_slab is not None:  # no views at all
         vol_slab.zero_()
         if vol_host is not None:
             vol_host.copy_(vol_slab)
@@ -645,6 +655,146 @@ def kslab_reconstruct_host(g, raw_host, vol_slab, vol_host, plan: SlabPlan, rank
                      exchange=exchange, peer=peer, streams=streams)
 
 
+# ------------------------------------------------------------------ fused projection split
+class ReduceSlabs:
+    """The owner slabs of the fused projection-split reduce, each mapped into every rank:
+    rank h's slab (its device memory; CUDA IPC makes it an NVLink peer mapping elsewhere)
+    holds slices k_bounds[h] .. k_bounds[h+1]-1 of the [Nz][Ny][Nx] volume.  ``create``
+    builds them over a process group, ``local`` all of them in one process (virtual ranks)."""
+
+    kind = "p2p-red"
+
+    def __init__(self, rank, world, bases, k_bounds, Ny, Nx, own=(), opened=()):
+        self.rank, self.world = rank, world
+        self.bases = [int(b) for b in bases]
+        self.k_bounds = list(k_bounds)
+        self.Ny, self.Nx = Ny, Nx
+        self._own, self._opened = list(own), list(opened)
+
+    @staticmethod
+    def _alloc(nk, Ny, Nx):
+        from .ifdk import peer_alloc
+
+        return peer_alloc(4 * max(nk, 1) * Ny * Nx)
+
+    @classmethod
+    def create(cls, group, rank, world, g, k_bounds):
+        import torch.distributed as dist
+
+        from .ifdk import peer_open
+
+        ptr, handle = cls._alloc(k_bounds[rank + 1] - k_bounds[rank], g.Ny, g.Nx)
+        handles = [None] * world
+        dist.all_gather_object(handles, handle, group=group)
+        bases, opened = [], []
+        for h in range(world):
+            if h == rank:
+                bases.append(ptr)
+            else:
+                q = peer_open(handles[h])
+                bases.append(q)
+                opened.append(q)
+        return cls(rank, world, bases, k_bounds, g.Ny, g.Nx, own=[ptr], opened=opened)
+
+    @classmethod
+    def local(cls, world, g, k_bounds):
+        ptrs = [cls._alloc(k_bounds[h + 1] - k_bounds[h], g.Ny, g.Nx)[0] for h in range(world)]
+        out = [cls(r, world, ptrs, k_bounds, g.Ny, g.Nx) for r in range(world)]
+        out[0]._own = ptrs  # rank 0's object frees them all
+        return out
+
+    def dests(self):
+        """(bases, first slices) of the non-empty slabs, for ifdk_backproject_reduce."""
+        kb = self.k_bounds
+        keep = [h for h in range(self.world) if kb[h + 1] > kb[h]]
+        return [self.bases[h] for h in keep], [kb[h] for h in keep]
+
+    def slab(self, h=None):
+        """Slab h (default: my own) as a device tensor [nk][Ny][Nx] over its mapping."""
+        from .ifdk import as_tensor
+
+        h = self.rank if h is None else h
+        return as_tensor(self.bases[h], (self.k_bounds[h + 1] - self.k_bounds[h], self.Ny, self.Nx))
+
+    def close(self):
+        from .ifdk import peer_close, peer_free
+
+        for q in self._opened:
+            peer_close(q)
+        for q in self._own:
+            peer_free(q)
+        self._opened, self._own = [], []
+
+
+def projection_split_fused(g, raw_local, blocks, slabs, group=None,
+                           filter_fn: Optional[Callable] = None,
+                           reduce_fn: Optional[Callable] = None,
+                           timings: Optional[dict] = None, mode: int = 0, zero: bool = True,
+                           sync: bool = True):
+    """Fused projection split on one rank: filter the rank's views (``blocks``: (first global
+    view, count) runs stored in raw_local, in order) and back-project them over the whole
+    volume, each 128-view partial sum added straight into its owner's slab
+    (``ifdk_backproject_reduce`` into ``slabs``, a ReduceSlabs).  zero / sync: zero the own
+    slab and order it before every rank's adds, and order every rank's adds before the
+    return (a device sync + a group barrier each); virtual ranks in one process pass False and
+    order the calls themselves.  Returns the own slab (a tensor over its mapping).  Equal to
+    one GPU up to fp32 summation order (the adds' order across ranks is not fixed)."""
+    import torch
+
+    from .ifdk import ifdk_backproject_reduce, ifdk_filter
+
+    if filter_fn is None:
+        def filter_fn(raw, out):
+            ifdk_filter(g, raw, out)
+    if reduce_fn is None:
+        bases, k0s = slabs.dests()
+
+        def reduce_fn(Qb, s0):
+            ifdk_backproject_reduce(g, Qb, s0, bases, k0s, 0, g.Nz, mode=mode)
+    barrier = _barrier_fn(group) if sync else (lambda: None)
+    cuda = raw_local.is_cuda
+    if zero:
+        slabs.slab().zero_()
+    if sync:
+        if cuda:
+            torch.cuda.synchronize()
+        barrier()  # every slab zeroed before any rank adds into it
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if (cuda and timings is not None) else None
+    if ev:
+        ev[0].record()
+    Q = torch.empty_like(raw_local)
+    if raw_local.shape[0] > 0:
+        filter_fn(raw_local, Q)
+    if ev:
+        ev[1].record()
+    off = 0
+    for s0, n in blocks:
+        if n > 0:
+            reduce_fn(Q[off:off + n], s0)
+        off += n
+    if ev:
+        ev[2].record()
+    if sync:
+        if cuda:
+            torch.cuda.synchronize()
+        barrier()  # every rank's adds have landed
+    if ev:
+        ev[2].synchronize()
+        timings.update({"filter_ms": ev[0].elapsed_time(ev[1]),
+                        "bp_reduce_ms": ev[1].elapsed_time(ev[2]),
+                        "wall_ms": ev[0].elapsed_time(ev[2])})
+    del Q
+    return slabs.slab()
+
+
+def _barrier_fn(group):
+    import torch.distributed as dist
+
+    if not dist.is_available() or not dist.is_initialized():
+        return lambda: None
+    return lambda: dist.barrier(group=group)
+
+
 # ----------------------------------------------------------------------------- R x C grid
 @dataclass(frozen=True)
 class GridPlan:
@@ -669,6 +819,12 @@ class GridPlan:
     def slab(self, r: int) -> tuple[int, int]:
         return SlabPlan(self.R, self.Nz, self.Np).slab(r)
 
+    def sub_bounds(self, r: int) -> list[int]:
+        """Split of slab r into C sub-slabs (the fused row reduce's owner slabs; multiples of
+        the 64-slice chunk where the slab is long enough): C + 1 slice boundaries."""
+        k0, nk = self.slab(r)
+        return [k0 + b for b in _split(nk, self.C, KC)]
+
     def sub_slab(self, rank: int) -> tuple[int, int]:
         """Slices (k0, n) rank owns at the end: sub-slab c of slab r, ceil(nk / C) slices
         each (the last ones may be shorter or empty)."""
@@ -692,16 +848,39 @@ def grid_groups(grid: GridPlan):
 def hybrid_reconstruct(g, raw_local, vol_sub, grid: GridPlan, rank: int, row_group, col_group,
                        filter_fn: Optional[Callable] = None, bp_fn: Optional[Callable] = None,
                        timings: Optional[dict] = None, exchange: str = "auto",
-                       peer: Optional[PeerExchange] = None):
+                       peer: Optional[PeerExchange] = None, slabs=None, mode: int = 0,
+                       streams=None):
     """R x C FDK on one rank.  raw_local: the rank's blocks of its column
     (grid.column_plan(c).local_views(r)) in order; vol_sub: [n][Ny][Nx] for
     grid.sub_slab(rank), overwritten.  Equal to one GPU up to fp32 summation order (the C
-    column partial sums are added by the reduce-scatter)."""
+    column partial sums are added by the reduce-scatter).
+
+    slabs (a ReduceSlabs over row r's C ranks, k_bounds = grid.sub_bounds(r)): the row sum is
+    fused into the back-projection instead -- every 128-view partial sum is added straight into
+    the owner of its sub-slab (ifdk_backproject_reduce), no partial slab and no reduce-scatter.
+    The owner slabs must be zeroed, and every rank's adds finished, around the call (the
+    caller orders them); vol_sub is unused and the own sub-slab (slabs.slab()) holds the result."""
     import torch
     import torch.distributed as dist
 
     r, c = grid.coords(rank)
     plan = grid.column_plan(c)
+    if slabs is not None:
+        from .ifdk import ifdk_backproject_reduce
+
+        kb = grid.sub_bounds(r)
+        if list(slabs.k_bounds) != kb:
+            raise ValueError("slabs must be the row's chunk-aligned sub-slabs (grid.sub_bounds)")
+
+        bases, k0s = slabs.dests()
+
+        def fused_bp(Qb, s0, vol, k0, v0, acc):
+            ifdk_backproject_reduce(g, Qb, s0, bases, k0s, k0=kb[0], nk=kb[-1] - kb[0], v0=v0,
+                                    mode=mode)
+
+        _pipeline(g, plan, r, None, col_group, filter_fn, fused_bp, timings,
+                  raw_local=raw_local, exchange=exchange, peer=peer, streams=streams)
+        return slabs.slab()
     k0, nk = grid.slab(r)
     q = -(-nk // grid.C)
     partial = raw_local.new_empty((q * grid.C, g.Ny, g.Nx))

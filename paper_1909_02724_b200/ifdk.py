@@ -40,6 +40,7 @@ EXPORTS = (
     "ifdk_peer_free",
     "ifdk_signal",
     "ifdk_wait",
+    "ifdk_backproject_reduce",
     "ifdk_backproject",
     "ifdk_backproject_alg2",
     "ifdk_backproject_alg4",
@@ -102,6 +103,9 @@ _lib.ifdk_wait.argtypes = [_vp, _i, ctypes.c_uint, ctypes.c_uint, _vp]
 _lib.ifdk_wait.restype = _i
 _lib.ifdk_backproject.argtypes = [_vp, _vp, _l, _l, _i, _i, _vp, _i, _i, _i, _vp]
 _lib.ifdk_backproject.restype = _i
+_lib.ifdk_backproject_reduce.argtypes = [_vp, _vp, _l, _l, _i, _i, _i, _i, _i,
+                                         ctypes.POINTER(_vp), ctypes.POINTER(_i), _i, _vp]
+_lib.ifdk_backproject_reduce.restype = _i
 _lib.ifdk_backproject_alg2.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _i, _i, _vp]
 _lib.ifdk_backproject_alg2.restype = _i
 _lib.ifdk_backproject_alg4.argtypes = [_vp, _vp, _l, _l, _vp, _i, _i, _vp]
@@ -302,6 +306,27 @@ def ifdk_backproject(g: Geometry, filtered, s0: int, vol, k0: int = 0, v0: int =
                                  filtered.shape[0], int(v0), filtered.shape[1],
                                  _dev_f32(vol, "vol"), int(k0), vol.shape[0],
                                  1 if accumulate else 0, _stream_ptr(stream)))
+
+
+def ifdk_backproject_reduce(g: Geometry, filtered, s0: int, dests, dest_k0, k0: int = 0,
+                            nk: int | None = None, v0: int = 0, mode: int = 0,
+                            stream=None) -> None:
+    """Fused projection-split BP: views s0.. (filtered [n][n_rows][Nu], rows v0..) over slices
+    k0..k0+nk-1, each 128-view partial sum ADDED (red.global.add, mode 0; multimem.red, mode
+    1) into the destination slab holding its slice: dests[d] (device pointers or tensors,
+    local or peer-mapped) holds slices dest_k0[d] .. dest_k0[d+1]-1."""
+    if filtered.dim() != 3 or filtered.shape[2] != g.Nu:
+        raise ValueError("filtered must be [n_views][n_rows][Nu]")
+    nk = g.Nz - k0 if nk is None else nk
+    ptrs = [d if isinstance(d, int) else _dev_f32(d, "dest") for d in dests]
+    if len(ptrs) != len(dest_k0):
+        raise ValueError("one start slice per destination slab")
+    arr = (_vp * len(ptrs))(*ptrs)
+    ks = (_i * len(dest_k0))(*[int(k) for k in dest_k0])
+    _check(_lib.ifdk_backproject_reduce(g.handle, _dev_f32(filtered, "filtered"), int(s0),
+                                        filtered.shape[0], int(v0), filtered.shape[1], int(k0),
+                                        int(nk), len(ptrs), arr, ks, int(mode),
+                                        _stream_ptr(stream)))
 
 
 def ifdk_backproject_alg2(g: Geometry, filtered, s0: int, vol, k0: int = 0,

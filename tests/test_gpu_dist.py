@@ -8,7 +8,10 @@
 * Virtual ranks (P = 2, 4, 8 in one process on one GPU): the production fused exchange
   layout, the scatter kernel's completion flags and the wait / signal kernels.
 * Two processes on ONE GPU (gloo for the host plumbing): the fused exchange across real
-  process boundaries (IPC-mapped buffers, signals between time-sliced contexts)."""
+  process boundaries (IPC-mapped buffers, signals between time-sliced contexts), and the
+  fused projection split's adds into a peer's IPC-mapped slab.
+* Virtual ranks for the fused reduce: the projection split at P = 1-8 and
+  R x C grids, back-projection adding straight into the owners' slabs."""
 import os
 import subprocess
 import sys
@@ -34,6 +37,7 @@ def test_kslab_under_torchrun_both_exchanges():
     assert out.count("bitwise=OK") == 3 * n, out[-3000:]  # auto, nccl, end-to-end host
     assert out.count("ORACLE-OK") == 2 * n, out[-3000:]
     assert out.count("PSPLIT") == n and "MISMATCH" not in out, out[-3000:]
+    assert out.count("PSFUSED") == n, out[-3000:]
     # on B200 the default exchange is the fused filter + peer-memory scatter
     assert out.count("exchange=auto used=p2p-fused") == n, out[-3000:]
 
@@ -64,4 +68,18 @@ def test_two_processes_one_gpu_fused_exchange():
     assert r.returncode == 0, out[-3000:]
     assert out.count("exchange=p2p used=p2p-fused bitwise=OK") == 2, out[-3000:]
     assert out.count("ORACLE-OK") == 2 and out.count("KSLAB-HOST") == 2, out[-3000:]
+    assert out.count("PSFUSED") == 2, out[-3000:]
     assert "MISMATCH" not in out, out[-3000:]
+
+
+def test_virtual_ranks_fused_reduce_and_grid():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "grid_check.py")],
+                       capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    print(out[-3000:])
+    assert r.returncode == 0, out[-3000:]
+    assert out.count("OK") >= 9 and "MISMATCH" not in out, out[-3000:]
+    assert out.count("FUSED projection split") == 4 and out.count("FUSED R x C grid") == 5

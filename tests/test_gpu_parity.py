@@ -218,8 +218,9 @@ def test_bp_walk_variants(torch_cuda, auto_variant):
         assert torch.equal(run("4"), run(walk)), walk
         assert torch.equal(run("4", 77, 54), run(walk, 77, 54)), walk
     tri = run("6")
-    assert torch.equal(tri, run("3"))
-    assert torch.equal(run("6", 77, 54), run("3", 77, 54))
+    for w in ("3", "9", "11"):  # pair patch; TMEM accumulators: one / two views per step
+        assert torch.equal(tri, run(w)), w
+        assert torch.equal(run("6", 77, 54), run(w, 77, 54)), w
     for a, b in ((0, 77), (77, 131), (131, 160)):  # partial chunks at every cut
         assert torch.equal(run("6", a, b - a), tri[a:b]), (a, b)
     og = oracle.OracleGeometry(**spec.geometry_args())
@@ -248,8 +249,9 @@ def test_bp_three_row_triple_walk(torch_cuda, auto_variant):
         return vol
 
     tri = run("7")
-    assert torch.equal(tri, run("8"))
-    assert torch.equal(run("7", 77, 54), run("8", 77, 54))
+    for w in ("8", "10", "12"):
+        assert torch.equal(tri, run(w)), w
+        assert torch.equal(run("7", 77, 54), run(w, 77, 54)), w
     for a, b in ((0, 77), (77, 131), (131, 200)):
         assert torch.equal(run("7", a, b - a), tri[a:b]), (a, b)
     og = oracle.OracleGeometry(**spec.geometry_args())
@@ -518,8 +520,43 @@ def test_bp_random_geometries(torch_cuda, seed):
 
 
 @pytest.mark.parametrize("family,walks,dims", [
-    ("4-row TRIPLE", ("6", "3"), (48, 96, 256, 48, 40, 256)),   # dv/dk in [0.60, 0.77]
-    ("3-row TRIPLE", ("7", "8"), (48, 96, 120, 48, 40, 256)),   # dv/dk in [0.28, 0.36]
+    ("4-row TRIPLE", ("6", "9", "11"), (600, 96, 256, 48, 40, 128)),
+    ("3-row TRIPLE", ("7", "10", "12"), (600, 96, 120, 48, 40, 128)),
+])
+def test_bp_tmem_walks_view_ranges(torch_cuda, auto_variant, family, walks, dims):
+    """The TMEM-accumulator walks (9 / 10: one view per step; 11 / 12: two views per step, a
+    one-view step where the first flush of the 128-view two-level sum falls on view 0 or at the
+    last view) are bitwise the register walk (6 / 7) for view ranges that start off the
+    128-view grid (s0 = 1, 37, 127, 128), have odd lengths and cross 256-view launch
+    boundaries -- and for one and two views.  The 600-view result matches the oracle."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_backproject, set_bp_variant
+
+    spec = _spec(*dims)
+    g = Geometry.from_spec(spec)
+    Qn = _oracle_Q32(spec, _phantom_E(spec))
+    Q = torch.from_numpy(Qn).cuda()
+
+    def run(w, s0, n):
+        set_bp_variant(int(w))
+        vol = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+        ifdk_backproject(g, Q[s0:s0 + n], s0, vol)
+        torch.cuda.synchronize()
+        return vol
+
+    for s0, n in ((0, 600), (1, 300), (37, 219), (127, 2), (128, 1), (1, 1), (0, 2), (5, 131)):
+        want = run(walks[0], s0, n)
+        for w in walks[1:]:
+            assert torch.equal(run(w, s0, n), want), (family, w, s0, n)
+    og = oracle.OracleGeometry(**spec.geometry_args())
+    ref = oracle.backproject_volume(og, Qn.astype(np.float64), s0=0, v0=0, k0=0, nk=spec.Nz)
+    assert_parity(run(walks[-1], 0, 600).cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL,
+                  f"bp {family} TMEM two-view walk, 600 views")
+
+
+@pytest.mark.parametrize("family,walks,dims", [
+    ("4-row TRIPLE", ("11", "6", "3", "9"), (48, 96, 256, 48, 40, 256)),  # dv/dk 0.60-0.77
+    ("3-row TRIPLE", ("12", "7", "8", "10"), (48, 96, 120, 48, 40, 256)),  # dv/dk 0.28-0.36
     ("PAIR", ("5", "4", "2"), (48, 96, 192, 48, 40, 256)),      # dv/dk in [0.45, 0.58]
 ])
 def test_bp_partial_chunks_far_into_the_chunk(torch_cuda, auto_variant, family, walks, dims):

@@ -20,8 +20,9 @@ import oracle  # noqa: E402
 import synth  # noqa: E402
 from parity_util import VOL_MAX_REL, VOL_RMSE, metrics  # noqa: E402
 from paper_1909_02724_b200 import Geometry, ifdk_reconstruct  # noqa: E402
-from paper_1909_02724_b200.dist import (SlabPlan, kslab_reconstruct,  # noqa: E402
-                                        kslab_reconstruct_host, projection_split_reconstruct)
+from paper_1909_02724_b200.dist import (ReduceSlabs, SlabPlan, kslab_reconstruct,  # noqa: E402
+                                        kslab_reconstruct_host, projection_split_fused,
+                                        projection_split_reconstruct)
 
 
 def main():
@@ -88,6 +89,18 @@ def main():
         bad += not ok
         print(f"PSPLIT rank {rank}/{world} max|d|/max|V|={err:.2e} {'OK' if ok else 'MISMATCH'}",
               flush=True)
+    # fused projection split: every rank's partial sums added straight into the owners' slabs
+    # (IPC-mapped: a peer's device memory), no partial volume, no reduce-scatter
+    slabs = ReduceSlabs.create(None, rank, world, g, plan.k_bounds)
+    own = projection_split_fused(g, raw, plan.local_views(rank), slabs)
+    err = float((own - ref[k0:k0 + nk]).abs().max() / ref.abs().max())
+    r_, m_ = metrics(own[idx[:, 2] - k0, idx[:, 1], idx[:, 0]].cpu().numpy(), want)
+    ok = err <= 1e-5 and r_ <= VOL_RMSE and m_ <= VOL_MAX_REL
+    bad += not ok
+    print(f"PSFUSED rank {rank}/{world} max|d|/max|V|={err:.2e} oracle relRMSE={r_:.2e} "
+          f"max={m_:.2e} {'OK' if ok else 'MISMATCH'}", flush=True)
+    dist.barrier()
+    slabs.close()
     dist.destroy_process_group()
     sys.exit(1 if bad else 0)
 

@@ -10,6 +10,10 @@ from paper_1909_02724_b200 import Geometry, ifdk_backproject, ifdk_filter  # noq
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 256
 nk = int(sys.argv[3]) if len(sys.argv) > 3 else None
+if len(sys.argv) > 4:  # BP walk (ifdk_set_bp_variant; bitwise-equal variants only)
+    from paper_1909_02724_b200 import set_bp_variant
+
+    set_bp_variant(int(sys.argv[4]))
 spec = synth.config(cfg)
 g = Geometry.from_spec(spec)
 E = torch.empty((n, spec.Nv, spec.Nu), device="cuda")
