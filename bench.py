@@ -574,6 +574,31 @@ def run_ours(args, spec, rank, world, local_rank):
 
     def measure_variants():
         nonlocal raw
+        if world > 1 and not args.no_variants:
+            # fused projection split: each rank back-projects its own views over the whole
+            # volume and adds every 128-view partial sum straight into the owner's slab over
+            # NVLink (ifdk_backproject_reduce into CUDA-IPC mappings) -- no partial volume, no
+            # reduce-scatter; needs only the rank's filtered views and its own slab
+            from paper_1909_02724_b200.dist import ReduceSlabs, projection_split_fused
+
+            torch.cuda.empty_cache()
+            slabs = ReduceSlabs.create(None, rank, world, g, plan.k_bounds)
+            projection_split_fused(g, raw, blocks, slabs)  # warm-up
+            tm = {}
+            projection_split_fused(g, raw, blocks, slabs, timings=tm)
+            fms = _max_over_ranks(tm["wall_ms"], world, dev)
+            own = slabs.slab()
+            vmax = _max_over_ranks(float(vol.abs().max()), world, dev)
+            dmax = float((own - vol).abs().max()) if own.shape == vol.shape else float("nan")
+            variants["projection_split_fused"] = {
+                "value": gups(spec, fms / 1e3), "unit": "GUPS", "ms_per_step": fms,
+                "filter_ms": _max_over_ranks(tm["filter_ms"], world, dev),
+                "bp_reduce_ms": _max_over_ranks(tm["bp_reduce_ms"], world, dev),
+                "max_abs_diff_vs_kslab_rel": _max_over_ranks(dmax, world, dev) / vmax,
+                "what": "ifdk_backproject_reduce: red.global.add into the owners' slabs"}
+            del own
+            dist.barrier()
+            slabs.close()
         if world > 1 and not args.no_variants and spec.Nz % world == 0:
             torch.cuda.empty_cache()
             need = 4 * (spec.Nz * spec.Ny * spec.Nx + n_local * spec.Nv * spec.Nu)
