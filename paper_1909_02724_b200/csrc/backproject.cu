@@ -87,13 +87,8 @@ __device__ __forceinline__ float* vol_voxel(const BPParams& p, int k, int j, int
 // added, or -- the fused reduce -- atomically added into the destination slab holding slice k
 // (slabs need not align with the 64-slice chunks; the order of the adds from different
 // launches / GPUs is not fixed, so fp32 rounding may differ).
-__device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, int j, int i,
-                                          float v, bool overwrite)
+__device__ __noinline__ void red_voxel(const BPParams& p, int k, int j, int i, float v)
 {
-    if (p.red == 0) {
-        *q = overwrite ? v : *q + v;
-        return;
-    }
     int d = 0;
     while (d + 1 < p.n_dest && k >= p.dest_k0[d + 1]) ++d;
     float* r = p.dest[d] + ((long)(k - p.dest_k0[d]) * p.Ny + j) * p.Nx + i;
@@ -102,6 +97,16 @@ __device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, in
     else
         asm volatile("multimem.red.relaxed.sys.global.add.f32 [%0], %1;" ::"l"(r), "f"(v)
                      : "memory");
+}
+
+// (the reduce path out of line: the flush's plain stores stay as compact as before)
+__device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, int j, int i,
+                                          float v, bool overwrite)
+{
+    if (p.red == 0)
+        *q = overwrite ? v : *q + v;
+    else
+        red_voxel(p, k, j, i, v);
 }
 
 struct __align__(16) Meta {

@@ -346,38 +346,43 @@ __device__ __forceinline__ void dft16(cx (&u)[16])
 // product of at most four table values (<= 3 roundings).
 constexpr int kTwL = 0, kTw16 = 4 * 256, kTwEntries = 4 * 256 + 4 * 16;
 
-__device__ __forceinline__ void twiddle_powers(cx (&w)[16], const cx* tw, int stride, int idx)
-{
-    w[1] = tw[idx];
-    w[2] = tw[stride + idx];
-    w[4] = tw[2 * stride + idx];
-    w[8] = tw[3 * stride + idx];
-    w[3] = cmulf(w[2], w[1]);
-    w[5] = cmulf(w[4], w[1]);
-    w[6] = cmulf(w[4], w[2]);
-    w[7] = cmulf(w[6], w[1]);
-    w[9] = cmulf(w[8], w[1]);
-    w[10] = cmulf(w[8], w[2]);
-    w[11] = cmulf(w[10], w[1]);
-    w[12] = cmulf(w[8], w[4]);
-    w[13] = cmulf(w[12], w[1]);
-    w[14] = cmulf(w[12], w[2]);
-    w[15] = cmulf(w[14], w[1]);
-}
 
 // One Stockham radix-16 pass of span P on the values u (= x[i + 256 j]) of thread i; writes
 // the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
+// u[j] *= w^(j e) for j = 1..15 from the four table powers w^(2^q e) (tw[q stride + idx]):
+// w^(j e) is a product of at most four of them (<= 3 roundings), each applied as soon as it
+// is formed, so few twiddles are live at once.
+__device__ __forceinline__ void apply_twiddles(cx (&u)[16], const cx* tw, int stride, int idx)
+{
+    const cx w1 = tw[idx], w2 = tw[stride + idx], w4 = tw[2 * stride + idx],
+             w8 = tw[3 * stride + idx];
+    u[1] = cmulf(u[1], w1);
+    u[2] = cmulf(u[2], w2);
+    u[4] = cmulf(u[4], w4);
+    u[8] = cmulf(u[8], w8);
+    u[3] = cmulf(u[3], cmulf(w2, w1));
+    u[5] = cmulf(u[5], cmulf(w4, w1));
+    const cx w6 = cmulf(w4, w2);
+    u[6] = cmulf(u[6], w6);
+    u[7] = cmulf(u[7], cmulf(w6, w1));
+    u[9] = cmulf(u[9], cmulf(w8, w1));
+    const cx w10 = cmulf(w8, w2);
+    u[10] = cmulf(u[10], w10);
+    u[11] = cmulf(u[11], cmulf(w10, w1));
+    const cx w12 = cmulf(w8, w4);
+    u[12] = cmulf(u[12], w12);
+    u[13] = cmulf(u[13], cmulf(w12, w1));
+    const cx w14 = cmulf(w12, w2);
+    u[14] = cmulf(u[14], w14);
+    u[15] = cmulf(u[15], cmulf(w14, w1));
+}
+
 template <int P, bool HALF = false>
 __device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* tw, int i)
 {
     static_assert(P == 1 || P == 16, "span-1 and span-16 passes");
     const int k = i & (P - 1);
-    if (P > 1) {
-        cx w[16];
-        twiddle_powers(w, tw + kTw16, 16, k);
-#pragma unroll
-        for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
-    }
+    if (P > 1) apply_twiddles(u, tw + kTw16, 16, k);
     dft16<HALF && P == 1>(u);
     const int base = (i - k) * 16 + k;
 #pragma unroll
@@ -393,6 +398,9 @@ __device__ __forceinline__ void load_in(cx (&u)[16], const cx* buf, int i)
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
 // X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
 // barrier: a buffer is rewritten only after the barrier that follows its last read.
+// (Measured alternative: one buffer and four barriers per transform, 80 registers and three
+// CTAs per SM -- 4.68 vs 4.69 ms per 256 config-4 views: the occupancy gain is spent on the
+// extra barriers, profiles/r2/ncu_filter_kernel_full_r2n.txt.)
 template <bool HALF = false>  // HALF: x[i + 256 j] = 0 for j >= 8 (a zero-padded 2048-sample row)
 __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const cx* tw, int i)
 {
@@ -403,10 +411,7 @@ __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const c
     __syncthreads();
     load_in(u, buf1, i);
     // span 256: k = i, outputs at i + 256 m stay in this thread
-    cx w[16];
-    twiddle_powers(w, tw + kTwL, 256, i);
-#pragma unroll
-    for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j]);
+    apply_twiddles(u, tw + kTwL, 256, i);
     dft16(u);
 }
 
@@ -637,7 +642,7 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
         int R = 1;
         while (R < 8 && 4096 / (2 * R) >= 2 * g->Nu - 1) R *= 2;
         const long groups = (total + 2 * R - 1) / (2 * R);
-        long grid = (long)sms * 2;
+        long grid = (long)sms * 2;  // persistent: the resident CTAs per SM
         if (grid > groups) grid = groups;
         // In-place filtering is safe with the prefetch: a group's rows are fetched before any
         // CTA writes them (each group belongs to one CTA) and never read again.  (A scatter
