@@ -80,13 +80,14 @@ def parity_sample(spec, n_random=1 << 20, central_rows=16, boundary_rows=8):
     """SURVEY 8(d)'s sample for configs 3-4: name -> (n, 3) int32 (i, j, k)."""
     rng = np.random.default_rng(SEED)
     cz = spec.Nz // 2
-    bnd = slab_boundaries(spec)
+    bnd = slab_boundaries(spec) if boundary_rows else []
     groups = {
         "random": np.stack([rng.integers(0, spec.Nx, n_random), rng.integers(0, spec.Ny, n_random),
                             rng.integers(0, spec.Nz, n_random)], 1),
         "central planes": _rows_of_planes(rng, spec, (cz - 1, cz, cz + 1), central_rows),
         "slab-boundary planes": _rows_of_planes(
-            rng, spec, [k for b in bnd for k in (b - 1, b)], boundary_rows),
+            rng, spec, [k for b in bnd for k in (b - 1, b)], boundary_rows) if bnd
+        else np.zeros((0, 3), np.int64),
         "corners": _corners(spec),
     }
     return {k: v.astype(np.int32) for k, v in groups.items()}
@@ -229,6 +230,29 @@ def test_config4_parity_set(torch_cuda):
     print(f"ORACLE config 4 sample: {osum.seconds:.1f} s, {osum.updates / osum.seconds / 1e9:.3f}"
           f" G updates/s")
     _report(spec, got, osum.acc, "config 4 parity set")
+
+
+def test_config3_noisy_stress_input(torch_cuda):
+    """SURVEY 8(d)'s stress input at full size: config 3 with E + N(0, (0.01 max E)^2) (seed 1234,
+    counter-based, synth.add_noise), which roughens Q and amplifies coordinate error (c-N1);
+    2^18 random voxels + the central planes against the oracle on the same noisy fp32 input."""
+    torch = torch_cuda
+    from paper_1909_02724_b200 import Geometry, ifdk_reconstruct
+
+    spec = synth.config(3)
+    g = Geometry.from_spec(spec)
+    E = _gen_raw(torch, spec, 0, spec.Np).cpu().numpy()
+    E = synth.add_noise(E, 0.01 * float(E.max()), seed=1234)
+    vol = torch.empty((spec.Nz, spec.Ny, spec.Nx), device="cuda")
+    ifdk_reconstruct(g, torch.from_numpy(E).cuda(), vol)
+    groups = parity_sample(spec, n_random=1 << 18, boundary_rows=0)
+    groups.pop("slab-boundary planes")
+    got = {n: _gather(torch, vol, ijk) for n, ijk in groups.items()}
+    del vol
+    bg = Background()
+    osum = _oracle_full_rows(torch, spec, groups, lambda b0, n: E[b0:b0 + n], bg)
+    bg.join()
+    _report(spec, got, osum.acc, "config 3 noisy stress input")
 
 
 # ------------------------------------------------------------------------------ config 5
