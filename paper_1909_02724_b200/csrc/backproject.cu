@@ -1759,8 +1759,8 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             };
             // two views per step want six boxes; where those do not fit three CTAs per SM
             // (tall or wide boxes) the one-view step (four boxes) is the faster choice
-            if ((w == 11 || w == 12) && 3 * (raw_smem(kRawBuf2) + 1024) > 228 * 1024) w -= 2;
-            const int nbuf = (w == 11 || w == 12) ? kRawBuf2 : kRawBuf;
+            if (w >= 11 && 3 * (raw_smem(kRawBuf2) + 1024) > 228 * 1024) w = w % 2 ? 9 : 10;
+            const int nbuf = w >= 11 ? kRawBuf2 : kRawBuf;
             smem = BW ? raw_smem(nbuf)
                       : 2 * (size_t)q.raw_bytes + 2 * sizeof(float2) * box_h * P2 +
                             kMetaRing * sizeof(Meta) + 16;
@@ -1814,8 +1814,8 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             return IFDK_OK;
         }
         if (w == 5) w = 4;
-        if (w == 6 || w == 9 || w == 11) w = 3;
-        if (w == 7 || w == 10 || w == 12) w = 8;
+        if (w == 6 || (w >= 9 && w % 2 == 1)) w = 3;
+        if (w == 7 || (w >= 9 && w % 2 == 0)) w = 8;
         if (w == 8) {
             switch (P2) {
                 case 24: return launch_t<64, 24, 8>(q, map, pt, tma, grid, smem, st);
@@ -1870,8 +1870,8 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     ifdk_status s = IFDK_OK;
     if (c1 > c0) s = run(walk, p.kb0 + c0 * KC, c1 - c0);
     // partial chunks: walk 4 for walk 5, 3 for 6, 8 for 7 (bitwise the same arithmetic)
-    const int wp = (walk == 6 || walk == 9 || walk == 11) ? 3
-                   : (walk == 7 || walk == 10 || walk == 12) ? 8 : 4;
+    const int wp = (walk == 6 || (walk >= 9 && walk % 2 == 1)) ? 3
+                   : (walk == 7 || (walk >= 9 && walk % 2 == 0)) ? 8 : 4;
     if (s == IFDK_OK && head) s = run(wp, p.kb0, 1);
     if (s == IFDK_OK && tail && (n_chunks - 1 > 0 || !head)) s = run(wp, p.kb0 + (n_chunks - 1) * KC, 1);
     return s;
@@ -1925,6 +1925,7 @@ void preload_bp_kernels()
     touch_kernel(bp_tmem2_kernel<72, 1>);
     touch_kernel(bp_tmem2_kernel<40, 2>);
     touch_kernel(bp_tmem2_kernel<72, 2>);
+
 
 }
 
