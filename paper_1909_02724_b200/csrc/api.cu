@@ -331,19 +331,66 @@ extern "C" ifdk_status ifdk_reconstruct(const ifdk_geometry* g, const float* raw
     cudaStream_t st = (cudaStream_t)stream;
     const size_t view_elems = (size_t)g->Nv * g->Nu;
     const long batch = n_views < kViewBatch ? (n_views > 0 ? n_views : 1) : kViewBatch;
-    float* Q = nullptr;
-    cudaError_t e = scratch_alloc(const_cast<ifdk_geometry*>(g), (void**)&Q,
-                                  sizeof(float) * view_elems * batch, st);
-    if (e != cudaSuccess) return fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(filtered scratch)");
-    if (n_views == 0) s = launch_backproject(g, Q, 0, 0, 0, g->Nv, vol_dev, 0, g->Nz, 0, st);
-    for (long b0 = 0; b0 < n_views && s == IFDK_OK; b0 += batch) {
-        const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
-        s = launch_filter(const_cast<ifdk_geometry*>(g), raw_dev + b0 * view_elems, Q, nb, 0,
-                          g->Nv, st);
-        if (s != IFDK_OK) break;
-        s = launch_backproject(g, Q, b0, nb, 0, g->Nv, vol_dev, 0, g->Nz, b0 > 0 ? 1 : 0, st);
+    ifdk_geometry* gm = const_cast<ifdk_geometry*>(g);
+    // Batch b + 1 is filtered on a side stream into the other of two scratch buffers while
+    // batch b is back-projected on `st` (the paper's filter / back-projection overlap, P:790-833,
+    // on one GPU): the filter kernels fill the SM slots the back-projection leaves free.
+    float* Q[2] = {nullptr, nullptr};
+    const long nbatch = (n_views + batch - 1) / batch;
+    cudaError_t e = scratch_alloc(gm, (void**)&Q[0], sizeof(float) * view_elems * batch, st);
+    if (e == cudaSuccess && nbatch > 1)
+        e = scratch_alloc(gm, (void**)&Q[1], sizeof(float) * view_elems * batch, st);
+    if (e != cudaSuccess) {
+        if (Q[0]) cudaFreeAsync(Q[0], st);
+        return fail(IFDK_ERR_OUT_OF_MEMORY, "cudaMallocAsync(filtered scratch)");
     }
-    cudaFreeAsync(Q, st);
+    if (n_views == 0) s = launch_backproject(g, Q[0], 0, 0, 0, g->Nv, vol_dev, 0, g->Nz, 0, st);
+    if (s == IFDK_OK && nbatch == 1) {  // nothing to overlap: no side stream (latency)
+        s = launch_filter(gm, raw_dev, Q[0], n_views, 0, g->Nv, st);
+        if (s == IFDK_OK) s = launch_backproject(g, Q[0], 0, n_views, 0, g->Nv, vol_dev, 0, g->Nz, 0, st);
+        cudaFreeAsync(Q[0], st);
+        return s;
+    }
+    cudaStream_t fs = nullptr;
+    cudaEvent_t ev[5] = {};  // start, filtered[2], consumed[2]
+    if (s == IFDK_OK && n_views > 0) {
+        if ((e = cudaStreamCreateWithFlags(&fs, cudaStreamNonBlocking)) != cudaSuccess)
+            s = cuda_fail(e, "cudaStreamCreate");
+        for (int q = 0; q < 5 && s == IFDK_OK; ++q)
+            if ((e = cudaEventCreateWithFlags(&ev[q], cudaEventDisableTiming)) != cudaSuccess)
+                s = cuda_fail(e, "cudaEventCreate");
+    }
+    if (s == IFDK_OK && n_views > 0) {
+        cudaEventRecord(ev[0], st);  // the caller's earlier work and the scratch allocations
+        cudaStreamWaitEvent(fs, ev[0], 0);
+        auto filter = [&](long b) {
+            const int q = (int)(b & 1);
+            const long b0 = b * batch;
+            const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
+            if (b >= 2) cudaStreamWaitEvent(fs, ev[3 + q], 0);  // BP of batch b - 2 read Q[q]
+            ifdk_status r = launch_filter(gm, raw_dev + b0 * view_elems, Q[q], nb, 0, g->Nv, fs);
+            cudaEventRecord(ev[1 + q], fs);
+            return r;
+        };
+        s = filter(0);
+        for (long b = 0; b < nbatch && s == IFDK_OK; ++b) {
+            const int q = (int)(b & 1);
+            const long b0 = b * batch;
+            const long nb = (n_views - b0) < batch ? (n_views - b0) : batch;
+            if (b + 1 < nbatch && (s = filter(b + 1)) != IFDK_OK) break;
+            cudaStreamWaitEvent(st, ev[1 + q], 0);
+            s = launch_backproject(g, Q[q], b0, nb, 0, g->Nv, vol_dev, 0, g->Nz, b0 > 0 ? 1 : 0, st);
+            cudaEventRecord(ev[3 + q], st);
+        }
+        // every filter launch joined before the scratch returns to the pool on `st`
+        cudaEventRecord(ev[0], fs);
+        cudaStreamWaitEvent(st, ev[0], 0);
+    }
+    for (int q = 0; q < 5; ++q)
+        if (ev[q]) cudaEventDestroy(ev[q]);
+    if (fs) cudaStreamDestroy(fs);
+    cudaFreeAsync(Q[0], st);
+    if (Q[1]) cudaFreeAsync(Q[1], st);
     return s;
 }
 
@@ -360,8 +407,8 @@ static ifdk_status reconstruct_host_impl(const ifdk_geometry* g, const float* ra
     const size_t plane = (size_t)g->Ny * g->Nx;
     const size_t vol_elems = (size_t)nks * plane;
     const long batch = n_views < kViewBatch ? (n_views > 0 ? n_views : 1) : kViewBatch;
-    // Two staging buffers: batch b+1 is copied on `cp` while batch b is filtered (in place)
-    // and back-projected on `st`.
+    // Two staging buffers: batch b+1 is copied and filtered (in place) on `cp` while batch b
+    // is back-projected on `st`.
     cudaStream_t cp = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
     float* buf[2] = {nullptr, nullptr};
@@ -412,6 +459,10 @@ static ifdk_status reconstruct_host_impl(const ifdk_geometry* g, const float* ra
                                   sizeof(float) * host_view_elems, sizeof(float) * view_elems, nb,
                                   cudaMemcpyHostToDevice, cp);
             if (ce != cudaSuccess && s == IFDK_OK) s = cuda_fail(ce, "cudaMemcpy2DAsync(views H2D)");
+            // filtered in place on the copy stream: overlaps the back-projection of batch b - 1
+            const ifdk_status fst = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb,
+                                                  v0, n_rows, cp);
+            if (fst != IFDK_OK && s == IFDK_OK) s = fst;
             cudaEventRecord(copied[q], cp);
         };
         if (nbatches > 0) enqueue_copy(0);
@@ -420,9 +471,7 @@ static ifdk_status reconstruct_host_impl(const ifdk_geometry* g, const float* ra
             const int q = (int)(b & 1);
             const long b0 = bat[b].first;
             const long nb = bat[b].second;
-            cudaStreamWaitEvent(st, copied[q], 0);
-            s = launch_filter(const_cast<ifdk_geometry*>(g), buf[q], buf[q], nb, v0, n_rows, st);
-            if (s != IFDK_OK) break;
+            cudaStreamWaitEvent(st, copied[q], 0);  // copied and filtered
             if (b + 1 < nbatches) {
                 s = launch_backproject(g, buf[q], b0, nb, v0, n_rows, vol, k0s, nks,
                                        b0 > 0 ? 1 : 0, st);

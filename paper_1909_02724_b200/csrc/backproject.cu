@@ -99,11 +99,14 @@ __device__ __noinline__ void red_voxel(const BPParams& p, int k, int j, int i, f
                      : "memory");
 }
 
-// (the reduce path out of line: the flush's plain stores stay as compact as before)
+// RED: the kernel instantiation may run the fused reduce (checked at run time, the reduce path
+// out of line).  The production walk (bp_tmem2_kernel) has a separate RED = false
+// instantiation without it: the mere call site cost it 1.2 % (2193 vs 2220 GUPS, config 4).
+template <bool RED = true>
 __device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, int j, int i,
                                           float v, bool overwrite)
 {
-    if (p.red == 0)
+    if (!RED || p.red == 0)
         *q = overwrite ? v : *q + v;
     else
         red_voxel(p, k, j, i, v);
@@ -1284,8 +1287,8 @@ __device__ __forceinline__ void walk_view_tmem(uint32_t tacc, uint32_t a0, const
 }
 
 // Flush: every slice's partial sum to the volume (mapping of flush_x2_triple), zeros back.
-template <int KC>
-__device__ __forceinline__ void flush_tmem_triple(uint32_t tacc, const BPParams& p, int i, int j,
+template <int KC, bool RED = true>
+__device__ __forceinline__ void flush_tmem_triple_r(uint32_t tacc, const BPParams& p, int i, int j,
                                                   int kb, bool overwrite, bool inside)
 {
     tm_wait_st();
@@ -1306,12 +1309,19 @@ __device__ __forceinline__ void flush_tmem_triple(uint32_t tacc, const BPParams&
                     const int kk = pi < 30 ? 6 * (pi / 3) + 3 * half + pi % 3
                                            : 60 + 2 * half + (pi - 30);
                     const float v = half ? hi2(a[m]) : lo2(a[m]);
-                    put_voxel(p, q0 + kk * plane, kb + kk, j, i, v, overwrite);
+                    put_voxel<RED>(p, q0 + kk * plane, kb + kk, j, i, v, overwrite);
                 }
             }
         }
         tm_st16(tacc + 16 * part, zero);
     }
+}
+
+template <int KC>
+__device__ __forceinline__ void flush_tmem_triple(uint32_t tacc, const BPParams& p, int i, int j,
+                                                  int kb, bool overwrite, bool inside)
+{
+    flush_tmem_triple_r<KC, true>(tacc, p, i, j, kb, overwrite, inside);
 }
 
 // TRI 1: 4-row TRIPLE (walk 9), 2: 3-row TRIPLE (walk 10).  Three CTAs per SM (80 registers,
@@ -1483,7 +1493,7 @@ __device__ __forceinline__ void walk_views_tmem2(uint32_t tacc, uint32_t a0, con
     }
 }
 
-template <int BW, int TRI>
+template <int BW, int TRI, bool RED = false>
 __global__ void __launch_bounds__(kThreads, 3)
     bp_tmem2_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
                     const __grid_constant__ PTable pt)
@@ -1573,7 +1583,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
             const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
             const bool ow = !p.accumulate && te <= first_flush;
-            flush_tmem_triple<KC>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
+            flush_tmem_triple_r<KC, RED>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
         }
         if (te + NB >= meta_next && meta_next < n) {  // boxes of the next eight views
             metas(meta_next);
@@ -1789,8 +1799,10 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         if (BW && w >= 9 && w <= 12) {
             auto k = w == 9    ? (BW == 40 ? bp_tmem_kernel<40, 1, 3> : bp_tmem_kernel<72, 1, 3>)
                      : w == 10 ? (BW == 40 ? bp_tmem_kernel<40, 2, 3> : bp_tmem_kernel<72, 2, 3>)
-                     : w == 11 ? (BW == 40 ? bp_tmem2_kernel<40, 1> : bp_tmem2_kernel<72, 1>)
-                               : (BW == 40 ? bp_tmem2_kernel<40, 2> : bp_tmem2_kernel<72, 2>);
+                     : w == 11 ? (q.red ? (BW == 40 ? bp_tmem2_kernel<40, 1, true> : bp_tmem2_kernel<72, 1, true>)
+                                        : (BW == 40 ? bp_tmem2_kernel<40, 1> : bp_tmem2_kernel<72, 1>))
+                               : (q.red ? (BW == 40 ? bp_tmem2_kernel<40, 2, true> : bp_tmem2_kernel<72, 2, true>)
+                                        : (BW == 40 ? bp_tmem2_kernel<40, 2> : bp_tmem2_kernel<72, 2>));
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp tmem)");
@@ -1925,6 +1937,10 @@ void preload_bp_kernels()
     touch_kernel(bp_tmem2_kernel<72, 1>);
     touch_kernel(bp_tmem2_kernel<40, 2>);
     touch_kernel(bp_tmem2_kernel<72, 2>);
+    touch_kernel(bp_tmem2_kernel<40, 1, true>);
+    touch_kernel(bp_tmem2_kernel<72, 1, true>);
+    touch_kernel(bp_tmem2_kernel<40, 2, true>);
+    touch_kernel(bp_tmem2_kernel<72, 2, true>);
 
 
 }
