@@ -16,7 +16,7 @@ import synth
 from paper_1909_02724_b200 import Geometry
 from paper_1909_02724_b200.dist import (GridPlan, SlabPlan, grid_groups, hybrid_reconstruct,
                                         kslab_reconstruct, kslab_reconstruct_host, plan_exchange,
-                                        projection_split_reconstruct)
+                                        projection_split_fused, projection_split_reconstruct)
 
 SPEC = synth.ConfigSpec("dist 36x40x36->24x20x40", 36, 40, 36, 24, 20, 40)
 
@@ -131,6 +131,57 @@ class HostPeerExchange:
             self.words[h][1, self.rank] += 1
 
 
+class HostReduceSlabs:
+    """Host fake of dist.ReduceSlabs for the gloo tests: every rank's owner slab in POSIX shared
+    memory, mapped by all ranks; the adds of the fused reduce (the GPU's red.global.add) are
+    serialised by a file lock."""
+
+    def __init__(self, tag, rank, world, k_bounds, Ny, Nx):
+        import fcntl
+        from multiprocessing import shared_memory
+
+        import torch.distributed as dist
+
+        self.rank, self.world, self.k_bounds = rank, world, list(k_bounds)
+        self.Ny, self.Nx, self._fcntl = Ny, Nx, fcntl
+        nk = [k_bounds[h + 1] - k_bounds[h] for h in range(world)]
+        self.shm = [None] * world
+        self.shm[rank] = shared_memory.SharedMemory(name=f"{tag}_{rank}", create=True,
+                                                    size=4 * max(nk[rank], 1) * Ny * Nx)
+        dist.barrier()
+        for h in range(world):
+            if h != rank:
+                self.shm[h] = shared_memory.SharedMemory(name=f"{tag}_{h}")
+        self.arr = [np.ndarray((nk[h], Ny, Nx), np.float32, buffer=self.shm[h].buf)
+                    for h in range(world)]
+        self.lock = open(f"/tmp/{tag}.lock", "w")
+
+    def slab(self, h=None):
+        return torch.from_numpy(self.arr[self.rank if h is None else h])
+
+    def add(self, vol, k0):
+        """Add a partial volume of slices k0.. into the owners' slabs (under the lock)."""
+        self._fcntl.flock(self.lock, self._fcntl.LOCK_EX)
+        try:
+            for h in range(self.world):
+                a, b = self.k_bounds[h], self.k_bounds[h + 1]
+                lo, hi = max(a, k0), min(b, k0 + vol.shape[0])
+                if hi > lo:
+                    self.arr[h][lo - a:hi - a] += vol[lo - k0:hi - k0]
+        finally:
+            self._fcntl.flock(self.lock, self._fcntl.LOCK_UN)
+
+    def close(self):
+        import torch.distributed as dist
+
+        dist.barrier()
+        self.arr = []
+        for h, m in enumerate(self.shm):
+            m.close()
+            if h == self.rank:
+                m.unlink()
+
+
 def _worker(rank, world, port, mode, out_q):
     import torch.distributed as dist
 
@@ -182,6 +233,25 @@ def _worker(rank, world, port, mode, out_q):
             vol = torch.empty((nk, SPEC.Ny, SPEC.Nx))
             hybrid_reconstruct(g, torch.from_numpy(mine), vol, grid, rank, rows[r], cols[c],
                                filter_fn=f, bp_fn=b)
+        elif mode == "psplit_fused":
+            # the fused projection split: each rank's partial sums added straight into the
+            # owners' slabs (here a shared-memory fake of ReduceSlabs), with its zero / barrier
+            # protocol; 8-view blocks dealt round-robin as on the GPU
+            plan = SlabPlan(world, SPEC.Nz, SPEC.Np, block=8)
+            k0, nk = plan.slab(rank)
+            blocks = plan.local_views(rank)
+            mine = np.concatenate([E[s0:s0 + n] for s0, n in blocks])
+            slabs = HostReduceSlabs(f"ifdkr_{port}", rank, world, plan.k_bounds, SPEC.Ny, SPEC.Nx)
+            try:
+                def reduce_fn(Qb, s0):
+                    part = oracle.backproject_volume(og, Qb.numpy().astype(np.float64), s0=s0)
+                    slabs.add(part.astype(np.float32), 0)
+
+                own = projection_split_fused(g, torch.from_numpy(mine), blocks, slabs,
+                                             filter_fn=f, reduce_fn=reduce_fn)
+                vol = own.clone()
+            finally:
+                slabs.close()
         else:
             n = SPEC.Np // world
             s0 = rank * n
@@ -200,7 +270,8 @@ def _worker(rank, world, port, mode, out_q):
 @pytest.mark.parametrize("world,mode", [(2, "kslab"), (3, "kslab"), (2, "kslab_host"),
                                         (2, "kslab_fused"), (3, "kslab_fused"),
                                         (4, "kslab_fused"),
-                                        (2, "projsplit"), (4, "grid22"), (3, "grid13"),
+                                        (2, "projsplit"), (2, "psplit_fused"),
+                                        (3, "psplit_fused"), (4, "grid22"), (3, "grid13"),
                                         (3, "grid31")])
 def test_multi_rank_matches_single(world, mode):
     ctx = mp.get_context("spawn")
@@ -258,6 +329,26 @@ def test_grid_plan_partitions():
             *grid.sub_slab(rank))))
         assert ks == list(range(2048)), (R, C)
         assert all(grid.slab(r)[0] % 64 == 0 for r in range(R))
+        # the fused row reduce's owner sub-slabs: partition each slab, chunk-aligned here
+        for r in range(R):
+            kb = grid.sub_bounds(r)
+            assert kb[0] == grid.slab(r)[0] and kb[-1] == sum(grid.slab(r))
+            assert all(a <= b for a, b in zip(kb, kb[1:])) and all(k % 64 == 0 for k in kb)
+
+
+def test_reduce_slab_destinations_skip_empty_slabs():
+    """ReduceSlabs.dests (what ifdk_backproject_reduce receives): the non-empty owner slabs, in
+    order, with strictly increasing first slices -- e.g. 8 ranks over 320 slices or over 100
+    (ranks without slices own an empty slab)."""
+    from paper_1909_02724_b200.dist import ReduceSlabs
+
+    for world, Nz in ((8, 320), (8, 100), (3, 2048), (1, 7)):
+        kb = SlabPlan(world, Nz, 64).k_bounds
+        rs = ReduceSlabs(0, world, list(range(1000, 1000 + world)), kb, 4, 4)
+        bases, k0s = rs.dests()
+        assert k0s[0] == 0 and all(a < b for a, b in zip(k0s, k0s[1:]))
+        assert len(bases) == sum(1 for h in range(world) if kb[h + 1] > kb[h])
+        assert all(kb[bases[i] - 1000] == k0s[i] for i in range(len(bases)))
 
 
 def test_band_exchange_volume_config4_p8():
