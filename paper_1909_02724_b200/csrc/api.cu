@@ -576,8 +576,6 @@ extern "C" void ifdk_geometry_destroy(ifdk_geometry* g)
     for (auto& d : g->dev) {
         if (d.Hs) cudaFree(d.Hs);
         if (d.tw) cudaFree(d.tw);
-        if (d.twA) cudaFree(d.twA);
-        if (d.twB) cudaFree(d.twB);
         if (d.pool) cudaMemPoolDestroy(d.pool);  // deferred until outstanding frees complete
     }
     delete g;

@@ -340,49 +340,68 @@ __device__ __forceinline__ void dft16(cx (&u)[16])
     for (int m = 0; m < 16; ++m) u[m] = v[m];
 }
 
-// Twiddle tables (host fp64, rounded once): TL[q][i] = w^(2^q i) for the span-256 pass
-// (thread i) and T16[q][k] = w^(16 2^q k) for the span-16 pass (k = i mod 16), each read with
-// consecutive indices across a warp (no bank conflicts).  w^(j e) for j = 1 .. 15 is then a
-// product of at most four table values (<= 3 roundings).
-constexpr int kTwL = 0, kTw16 = 4 * 256, kTwEntries = 4 * 256 + 4 * 16;
-
-
-// One Stockham radix-16 pass of span P on the values u (= x[i + 256 j]) of thread i; writes
-// the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
-// u[j] *= w^(j e) for j = 1..15 from the four table powers w^(2^q e) (tw[q stride + idx]):
-// w^(j e) is a product of at most four of them (<= 3 roundings), each applied as soon as it
-// is formed, so few twiddles are live at once.
-__device__ __forceinline__ void apply_twiddles(cx (&u)[16], const cx* tw, int stride, int idx)
+// Per-thread twiddles in tensor memory.  Thread i's span-16 pass multiplies u[j] by w^(16 j k)
+// (k = i mod 16) and its span-256 pass by w^(j i), j = 1..15, w = e^(-2 pi i / 4096): the same
+// 2 x 15 complex values for every row group the (persistent) thread transforms.  They are read
+// once per launch from the host's table of w^e (fp64, rounded once) and kept in the CTA's
+// tensor memory -- 128 columns; warp w owns lanes 32 (w mod 4) .. +31 and columns 64 (w / 4)
+// .. +63: columns 0..29 hold the span-16 set, 32..61 the span-256 set -- so a twiddled pass
+// costs one tcgen05.ld of 32 registers (issued before the exchange's shared loads, awaited
+// after them) and 15 complex multiplies.  (Round 2's first form read four power tables per
+// pass and composed the other eleven powers: 22 % of the kernel's instructions, r2x capture.)
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, cx (&w)[16])
 {
-    const cx w1 = tw[idx], w2 = tw[stride + idx], w4 = tw[2 * stride + idx],
-             w8 = tw[3 * stride + idx];
-    u[1] = cmulf(u[1], w1);
-    u[2] = cmulf(u[2], w2);
-    u[4] = cmulf(u[4], w4);
-    u[8] = cmulf(u[8], w8);
-    u[3] = cmulf(u[3], cmulf(w2, w1));
-    u[5] = cmulf(u[5], cmulf(w4, w1));
-    const cx w6 = cmulf(w4, w2);
-    u[6] = cmulf(u[6], w6);
-    u[7] = cmulf(u[7], cmulf(w6, w1));
-    u[9] = cmulf(u[9], cmulf(w8, w1));
-    const cx w10 = cmulf(w8, w2);
-    u[10] = cmulf(u[10], w10);
-    u[11] = cmulf(u[11], cmulf(w10, w1));
-    const cx w12 = cmulf(w8, w4);
-    u[12] = cmulf(u[12], w12);
-    u[13] = cmulf(u[13], cmulf(w12, w1));
-    const cx w14 = cmulf(w12, w2);
-    u[14] = cmulf(u[14], w14);
-    u[15] = cmulf(u[15], cmulf(w14, w1));
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+#pragma unroll
+    for (int m = 0; m < 16; ++m) w[m] = mk(__uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
 }
 
+__device__ __forceinline__ void tm_st32(uint32_t taddr, const cx (&w)[16])
+{
+    float r[32];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        r[2 * m] = re_(w[m]);
+        r[2 * m + 1] = im_(w[m]);
+    }
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31, %32};" ::"r"(taddr),
+        "f"(r[0]), "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7]),
+        "f"(r[8]), "f"(r[9]), "f"(r[10]), "f"(r[11]), "f"(r[12]), "f"(r[13]), "f"(r[14]),
+        "f"(r[15]), "f"(r[16]), "f"(r[17]), "f"(r[18]), "f"(r[19]), "f"(r[20]), "f"(r[21]),
+        "f"(r[22]), "f"(r[23]), "f"(r[24]), "f"(r[25]), "f"(r[26]), "f"(r[27]), "f"(r[28]),
+        "f"(r[29]), "f"(r[30]), "f"(r[31]));
+}
+
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void apply_twiddles(cx (&u)[16], const cx (&w)[16])
+{
+#pragma unroll
+    for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j - 1]);
+}
+
+// One Stockham radix-16 pass of span P on the values u (= x[i + 256 j], twiddled) of thread i;
+// writes the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
 template <int P, bool HALF = false>
-__device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, const cx* tw, int i)
+__device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, int i)
 {
     static_assert(P == 1 || P == 16, "span-1 and span-16 passes");
     const int k = i & (P - 1);
-    if (P > 1) apply_twiddles(u, tw + kTw16, 16, k);
     dft16<HALF && P == 1>(u);
     const int base = (i - k) * 16 + k;
 #pragma unroll
@@ -397,21 +416,29 @@ __device__ __forceinline__ void load_in(cx (&u)[16], const cx* buf, int i)
 
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
 // X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
-// barrier: a buffer is rewritten only after the barrier that follows its last read.
-// (Measured alternative: one buffer and four barriers per transform, 80 registers and three
-// CTAs per SM -- 4.68 vs 4.69 ms per 256 config-4 views: the occupancy gain is spent on the
-// extra barriers, profiles/r2/ncu_filter_kernel_full_r2n.txt.)
+// barrier: a buffer is rewritten only after the barrier that follows its last read.  tw: this
+// thread's tensor-memory twiddle columns.
 template <bool HALF = false>  // HALF: x[i + 256 j] = 0 for j >= 8 (a zero-padded 2048-sample row)
-__device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const cx* tw, int i)
+__device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, uint32_t tw, int i)
 {
-    pass_out<1, HALF>(u, buf0, tw, i);
+    pass_out<1, HALF>(u, buf0, i);
     __syncthreads();
-    load_in(u, buf0, i);
-    pass_out<16>(u, buf1, tw, i);
+    {
+        cx w[16];
+        tm_ld32(tw, w);  // span-16 twiddles, in flight during the exchange's loads
+        load_in(u, buf0, i);
+        tm_wait_ld();
+        apply_twiddles(u, w);
+    }
+    pass_out<16>(u, buf1, i);
     __syncthreads();
-    load_in(u, buf1, i);
-    // span 256: k = i, outputs at i + 256 m stay in this thread
-    apply_twiddles(u, tw + kTwL, 256, i);
+    {
+        cx w[16];
+        tm_ld32(tw + 32, w);  // span 256: k = i, outputs at i + 256 m stay in this thread
+        load_in(u, buf1, i);
+        tm_wait_ld();
+        apply_twiddles(u, w);
+    }
     dft16(u);
 }
 
@@ -419,10 +446,19 @@ __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, const c
 
 // ASYNC (rows 16-byte aligned, Nu % 4 == 0): the next group's rows are fetched into a shared
 // staging buffer by 1-D bulk copies (the TMA engine; one instruction per row, completion on an
-// mbarrier) while the current group is transformed, hiding HBM latency.
+// mbarrier) while the current group is transformed, hiding HBM latency.  The staging slots are
+// zeroed once per launch: a copy writes the first N_u floats of a slot, so the padding after
+// them stays zero and the rows are read without masks.
 constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
-constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float2) * f4k::kTwEntries +
-                            sizeof(float) * 2052 + sizeof(float) * 2 * kF4kStage + 16;
+constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float) * 2052 +
+                            sizeof(float) * 2 * kF4kStage + 16;
+
+// Destination row of view t, detector row v in band d, or nullptr if v is outside the band.
+__device__ __forceinline__ float* dest_row_tv(const FilterParams& p, long t, int v, int d)
+{
+    if (v < p.lo[d] || v > p.hi[d]) return nullptr;
+    return p.base[d] + (t * (p.hi[d] - p.lo[d] + 1) + (v - p.lo[d])) * (long)p.Nu;
+}
 
 // R row pairs per transform (multi-row packing): with N_u <= 2048 / R every row's linear
 // convolution needs only a 2 N_u - 1 window of the length-4096 circular one, so R rows share
@@ -442,39 +478,73 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
     extern __shared__ __align__(16) unsigned char fsm[];
     cx* const buf = reinterpret_cast<cx*>(fsm);  // 2 x (L + L/16) (padded)
     cx* const bufB = buf + (L + L / 16);
-    cx* const tw = bufB + (L + L / 16);           // kTwEntries
-    float* const Hs = reinterpret_cast<float*>(tw + kTwEntries);  // L/2 + 1 (2052 slots)
-    float* const stage = Hs + 2052;                                // ROWS rows of SLOT_F
+    float* const Hs = reinterpret_cast<float*>(bufB + (L + L / 16));  // L/2 + 1 (2052 slots)
+    float* const stage = Hs + 2052;                                    // ROWS rows of SLOT_F
     uint64_t* const sbar = reinterpret_cast<uint64_t*>(stage + 2 * kF4kStage);  // staging barrier
-    const int i = threadIdx.x;
-    for (int e = i; e < kTwEntries; e += T) tw[e] = reinterpret_cast<const cx*>(tw_g)[e];
+    uint32_t* const tslot = reinterpret_cast<uint32_t*>(sbar + 1);             // TMEM address
+    const int i = threadIdx.x, warp = i >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                         smem_u32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
     for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
+    if (ASYNC)
+        for (int e = i; e < 2 * kF4kStage; e += T) stage[e] = 0.f;
     const long n_groups = (p.n_rows_total + ROWS - 1) / ROWS;
     if (ASYNC && i == 0) {
         mbar_init(sbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmw = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    {
+        const cx* twc = reinterpret_cast<const cx*>(tw_g);  // w^e, e = 0 .. 4095
+        cx w[16];
+        w[15] = 0ull;
+#pragma unroll
+        for (int j = 1; j < 16; ++j) w[j - 1] = twc[(16 * j * (i & 15)) & 4095];
+        tm_st32(tmw, w);
+#pragma unroll
+        for (int j = 1; j < 16; ++j) w[j - 1] = twc[(j * i) & 4095];
+        tm_st32(tmw + 32, w);
+        tm_wait_st();
+    }
     auto prefetch = [&](long gi) {  // one thread: the group's rows by 1-D bulk copies
         if (!ASYNC || gi >= n_groups || i != 0) return;
         const long r0 = ROWS * gi;
         const int nrow = (int)min((long)ROWS, p.n_rows_total - r0);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic reads
+        // a partial last group: the missing rows' slots are zeroed (they share the transforms)
+        for (int r = nrow; r < ROWS; ++r)
+            for (int n = 0; n < SLOT_F; ++n) stage[r * SLOT_F + n] = 0.f;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after the generic accesses
         mbar_expect_tx(sbar, (uint32_t)(nrow * p.Nu * 4));
         for (int r = 0; r < nrow; ++r)
             bulk_load(stage + r * SLOT_F, p.raw + (r0 + r) * p.Nu, (uint32_t)(p.Nu * 4), sbar);
     };
     prefetch(blockIdx.x);
+    // (view, detector row) of the group's first row, stepped without a division per group
+    const int nr = p.n_rows;
+    const long stepR = (long)ROWS * gridDim.x;
+    const long sq = stepR / nr;
+    const int sr = (int)(stepR - sq * nr);
+    long t0 = (long)ROWS * blockIdx.x / nr;
+    int vr0 = (int)((long)ROWS * blockIdx.x - t0 * nr);
     uint32_t sphase = 0;
     for (long gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
         const long r0 = ROWS * gi;
-        // per slot s: rows A = r0 + 2s (real part), B = r0 + 2s + 1 (imaginary part)
+        // D^2 + vh^2 of rows A = r0 + 2 s (real part) and B = r0 + 2 s + 1 (imaginary part)
         float dA[R], dB[R];
 #pragma unroll
         for (int sl = 0; sl < R; ++sl) {
-            const long rA = r0 + 2 * sl, rB = rA + 1;
-            const float vhA = ((float)(p.v0 + (int)(rA % p.n_rows)) - p.cv) * p.Dv;
-            const float vhB = ((float)(p.v0 + (int)(rB % p.n_rows)) - p.cv) * p.Dv;
+            int vA = vr0 + 2 * sl, vB = vA + 1;
+            while (vA >= nr) vA -= nr;
+            while (vB >= nr) vB -= nr;
+            const float vhA = ((float)(p.v0 + vA) - p.cv) * p.Dv;
+            const float vhB = ((float)(p.v0 + vB) - p.cv) * p.Dv;
             dA[sl] = p.D2 + vhA * vhA;
             dB[sl] = p.D2 + vhB * vhB;
         }
@@ -490,23 +560,22 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
         // >= D^2, never denormal) -- far below the filter tolerance.
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-            if (R == 1 && j >= 8) {  // n = i + 256 j >= 2048 >= N_u: the zero padding
+            const int sl = j / SJ, jj = j % SJ;
+            if (jj >= SJ / 2) {  // n >= S / 2 >= N_u: the zero padding of the slot
                 u[j] = 0ull;
                 continue;
             }
-            const int sl = j / SJ;
-            const int n = i + (j % SJ) * T;
-            const long rA = r0 + 2 * sl, rB = rA + 1;
+            const int n = i + jj * T;
             float ea = 0.f, eb = 0.f;
-            if (ASYNC) {  // read clamped into the row's staging slot; select, no branch
-                const int nc = n < SLOT_F ? n : SLOT_F - 1;  // n >= SLOT_F >= N_u: padding
-                const float sa = stage[(2 * sl) * SLOT_F + nc];
-                const float sb = stage[(2 * sl + 1) * SLOT_F + nc];
-                ea = (n < p.Nu && rA < p.n_rows_total) ? sa : 0.f;
-                eb = (n < p.Nu && rB < p.n_rows_total) ? sb : 0.f;
-            } else if (n < p.Nu && rA < p.n_rows_total) {
-                ea = __ldg(p.raw + rA * p.Nu + n);
-                if (rB < p.n_rows_total) eb = __ldg(p.raw + rB * p.Nu + n);
+            if (ASYNC) {
+                ea = stage[(2 * sl) * SLOT_F + n];
+                eb = stage[(2 * sl + 1) * SLOT_F + n];
+            } else {
+                const long rA = r0 + 2 * sl, rB = rA + 1;
+                if (n < p.Nu && rA < p.n_rows_total) {
+                    ea = __ldg(p.raw + rA * p.Nu + n);
+                    if (rB < p.n_rows_total) eb = __ldg(p.raw + rB * p.Nu + n);
+                }
             }
             const float uh = ((float)n - p.cu) * p.Du;
             const cx q = cfma2(mk(uh, uh), mk(uh, uh), mk(dA[sl], dB[sl]));
@@ -514,39 +583,75 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
         }
         __syncthreads();  // staging read and buffers free: fetch the next group meanwhile
         prefetch(gi + gridDim.x);
-        fft4096<R == 1>(u, buf, bufB, tw, i);
+        fft4096<R == 1>(u, buf, bufB, tmw, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
+        // X[f], f = i + 256 m, takes H[f] for m < 8 and H[L - f] for m >= 8 (f = L/2 only for
+        // m = 8, i = 0, where both are H[L/2]).
+        {
+            const float* hp = Hs + i;
+            const float* hn = Hs + (L - i);
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-            const int f = i + m * T;
-            const float h = Hs[f <= L / 2 ? f : L - f];
-            u[m] = cmul2(u[m], mk(h, -h));
+            for (int m = 0; m < 16; ++m) {
+                const float h = m < 8 ? hp[256 * m] : hn[-256 * m];
+                u[m] = cmul2(u[m], mk(h, -h));
+            }
         }
-        fft4096(u, buf, bufB, tw, i);  // buf's last reader was before bufB's barrier
+        fft4096(u, buf, bufB, tmw, i);  // buf's last reader was before bufB's barrier
         // Q = conj(Z): real -> row A, -imag -> row B of each slot, samples 0..Nu-1 (to every
         // destination band that holds the row when scattering).
-        const int nd = p.n_dest > 0 ? p.n_dest : 1;
-        for (int d = 0; d < nd; ++d) {
+        if (p.n_dest == 0) {
 #pragma unroll
             for (int sl = 0; sl < R; ++sl) {
-                const long rA = r0 + 2 * sl, rB = rA + 1;
+                const long rA = r0 + 2 * sl;
                 if (rA >= p.n_rows_total) break;
-                float* qA = p.n_dest > 0 ? dest_row(p, rA, d) : p.out + rA * p.Nu;
-                float* qB = rB >= p.n_rows_total ? nullptr
-                            : p.n_dest > 0      ? dest_row(p, rB, d)
-                                                : p.out + rB * p.Nu;
+                const bool hasB = rA + 1 < p.n_rows_total;
+                float* const qA = p.out + rA * p.Nu;
+                float* const qB = qA + p.Nu;
 #pragma unroll
-                for (int jj = 0; jj < (R > 1 ? SJ : 8); ++jj) {
-                    const int m = sl * SJ + jj;
+                for (int jj = 0; jj < SJ / 2; ++jj) {
                     const int n = i + jj * T;
                     if (n < p.Nu) {
-                        if (qA) qA[n] = re_(u[m]);
-                        if (qB) qB[n] = -im_(u[m]);
+                        qA[n] = re_(u[sl * SJ + jj]);
+                        if (hasB) qB[n] = -im_(u[sl * SJ + jj]);
+                    }
+                }
+            }
+        } else {
+            for (int d = 0; d < p.n_dest; ++d) {
+#pragma unroll
+                for (int sl = 0; sl < R; ++sl) {
+                    const long rA = r0 + 2 * sl, rB = rA + 1;
+                    if (rA >= p.n_rows_total) break;
+                    int vA = vr0 + 2 * sl, vB = vA + 1;
+                    long tA = t0, tB = t0;
+                    while (vA >= nr) { vA -= nr; ++tA; }
+                    while (vB >= nr) { vB -= nr; ++tB; }
+                    float* qA = dest_row_tv(p, tA, p.v0 + vA, d);
+                    float* qB = rB < p.n_rows_total ? dest_row_tv(p, tB, p.v0 + vB, d) : nullptr;
+#pragma unroll
+                    for (int jj = 0; jj < SJ / 2; ++jj) {
+                        const int n = i + jj * T;
+                        if (n < p.Nu) {
+                            if (qA) qA[n] = re_(u[sl * SJ + jj]);
+                            if (qB) qB[n] = -im_(u[sl * SJ + jj]);
+                        }
                     }
                 }
             }
         }
+        t0 += sq;
+        vr0 += sr;
+        if (vr0 >= nr) {
+            vr0 -= nr;
+            ++t0;
+        }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tslot)
+                     : "memory");
     signal_done(p);
 }
 
@@ -590,24 +695,6 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
             cudaMemcpy(D.Hs, g->Hs.data(), sizeof(float) * (L / 2 + 1), cudaMemcpyHostToDevice);
             e = cudaMemcpy(D.tw, g->tw.data(), sizeof(float2) * L, cudaMemcpyHostToDevice);
             if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(filter tables)");
-            if (L == 4096) {
-                // f4k twiddle tables: TL[q][i] = w^(2^q i), T16[q][k] = w^(16 2^q k)
-                std::vector<float> a(2 * f4k::kTwEntries);
-                auto put = [&](int slot, long ex) {
-                    const long t = ex % 4096;
-                    a[2 * slot] = g->tw[2 * t];
-                    a[2 * slot + 1] = g->tw[2 * t + 1];
-                };
-                for (int q = 0; q < 4; ++q)
-                    for (int ii = 0; ii < 256; ++ii) put(f4k::kTwL + q * 256 + ii, (long)(1 << q) * ii);
-                for (int q = 0; q < 4; ++q)
-                    for (int k = 0; k < 16; ++k) put(f4k::kTw16 + q * 16 + k, 16L * (1 << q) * k);
-                if ((e = cudaMalloc(&D.twA, sizeof(float2) * f4k::kTwEntries)) != cudaSuccess)
-                    return cuda_fail(e, "cudaMalloc(twiddles)");
-                e = cudaMemcpy(D.twA, a.data(), sizeof(float2) * f4k::kTwEntries,
-                               cudaMemcpyHostToDevice);
-                if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(filter tables)");
-            }
         }
     }
     const long total = n_views * (long)n_rows;
@@ -656,7 +743,7 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
                      : pick(filter_f4k_kernel<true, 1>, filter_f4k_kernel<false, 1>);
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4kSmem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
-        k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].twA, g->dev[dev].Hs);
+        k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].tw, g->dev[dev].Hs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "filter_f4k_kernel launch");
         count_launch();

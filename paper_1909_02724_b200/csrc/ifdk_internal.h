@@ -25,8 +25,6 @@ struct ifdk_geometry {
     struct Dev {
         float* Hs = nullptr;
         float2* tw = nullptr;
-        float2* twA = nullptr;  // length-4096 kernel: power tables w^(2^q i), w^(16 2^q k)
-        float2* twB = nullptr;  // unused (kept so api.cu's cleanup stays uniform)
         // stream-ordered pool for ifdk_reconstruct* scratch; keeps its memory between calls
         // (release threshold = max) and is destroyed with the geometry
         cudaMemPool_t pool = nullptr;
