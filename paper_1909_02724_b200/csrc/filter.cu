@@ -208,7 +208,6 @@ namespace f4k {
 
 constexpr int L = 4096, T = 256;
 
-__device__ __forceinline__ int padx(int q) { return q + (q >> 4); }  // 1 pad word per 16
 
 // Complex values ride in one 64-bit register pair (re, im) and every butterfly is a Blackwell
 // packed fp32x2 instruction: a complex add is one FADD2, a multiplication by -i is free (the
@@ -395,47 +394,55 @@ __device__ __forceinline__ void apply_twiddles(cx (&u)[16], const cx (&w)[16])
     for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j - 1]);
 }
 
-// One Stockham radix-16 pass of span P on the values u (= x[i + 256 j], twiddled) of thread i;
-// writes the outputs to buf[(i - k) 16 + k + m P], k = i mod P.
-template <int P, bool HALF = false>
-__device__ __forceinline__ void pass_out(cx (&u)[16], cx* buf, int i)
-{
-    static_assert(P == 1 || P == 16, "span-1 and span-16 passes");
-    const int k = i & (P - 1);
-    dft16<HALF && P == 1>(u);
-    const int base = (i - k) * 16 + k;
-#pragma unroll
-    for (int m = 0; m < 16; ++m) buf[padx(base + m * P)] = u[m];
-}
-
-__device__ __forceinline__ void load_in(cx (&u)[16], const cx* buf, int i)
-{
-#pragma unroll
-    for (int j = 0; j < 16; ++j) u[j] = buf[padx(i + j * T)];
-}
+// The two exchanges of a transform go through buffers in natural order with one pad value per
+// 16 (q -> q + q / 16; 64-bit complex values, 32 banks of 4 B; a 64-bit access is served per
+// half-warp).  The span-1 pass of thread i writes X1[16 i + m] at 17 i + m, the span-16 pass of
+// thread i (h = i / 16, k = i mod 16) writes q = 256 h + k + 16 m at 272 h + k + 17 m, and both
+// later passes read x[i + 256 j] at i + i / 16 + 272 j: every half-warp covers the 32 banks
+// once.  (Measured alternatives, r2z: two pads per 16 with the span-1 outputs as 128-bit
+// stores -- the u pairs are not allocated as aligned quads, so every store cost four moves;
+// and a transposed second buffer read as 128-bit loads, which puts a 2-way conflict on the
+// span-16 stores: 4.28 vs 4.01 ms per 256 config-4 views.)
+constexpr int kXBuf = 4096 + 256;  // complex slots per exchange buffer
 
 // Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
-// X[i + 256 m].  The two exchanges go through two different buffers, so each needs one
-// barrier: a buffer is rewritten only after the barrier that follows its last read.  tw: this
-// thread's tensor-memory twiddle columns.
+// X[i + 256 m].  Three radix-16 Stockham passes of spans 1, 16, 256 (decimation in time: pass
+// of span P twiddles its inputs by w^(j P k'), k' = i mod P, then takes a 16-point DFT).  The
+// two exchanges go through two different buffers, so each needs one barrier: a buffer is
+// rewritten only after the barrier that follows its last read.  tw: this thread's
+// tensor-memory twiddle columns.
 template <bool HALF = false>  // HALF: x[i + 256 j] = 0 for j >= 8 (a zero-padded 2048-sample row)
 __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, uint32_t tw, int i)
 {
-    pass_out<1, HALF>(u, buf0, i);
+    dft16<HALF>(u);  // span 1
+    {
+        cx* const o = buf0 + 17 * i;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) o[m] = u[m];
+    }
     __syncthreads();
     {
         cx w[16];
         tm_ld32(tw, w);  // span-16 twiddles, in flight during the exchange's loads
-        load_in(u, buf0, i);
+        const cx* const in = buf0 + i + (i >> 4);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) u[j] = in[272 * j];
         tm_wait_ld();
         apply_twiddles(u, w);
     }
-    pass_out<16>(u, buf1, i);
+    dft16(u);  // span 16
+    {
+        cx* const o = buf1 + 272 * (i >> 4) + (i & 15);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) o[17 * m] = u[m];
+    }
     __syncthreads();
     {
         cx w[16];
         tm_ld32(tw + 32, w);  // span 256: k = i, outputs at i + 256 m stay in this thread
-        load_in(u, buf1, i);
+        const cx* const in = buf1 + i + (i >> 4);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) u[j] = in[272 * j];
         tm_wait_ld();
         apply_twiddles(u, w);
     }
@@ -450,7 +457,7 @@ __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, uint32_
 // zeroed once per launch: a copy writes the first N_u floats of a slot, so the padding after
 // them stays zero and the rows are read without masks.
 constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
-constexpr size_t kF4kSmem = 2 * sizeof(float2) * (4096 + 256) + sizeof(float) * 2052 +
+constexpr size_t kF4kSmem = 2 * sizeof(float2) * f4k::kXBuf + sizeof(float) * 2052 +
                             sizeof(float) * 2 * kF4kStage + 16;
 
 // Destination row of view t, detector row v in band d, or nullptr if v is outside the band.
@@ -476,9 +483,9 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
     constexpr int ROWS = 2 * R;         // rows per transform
     constexpr int SLOT_F = 4096 / ROWS; // staged floats per row (>= N_u)
     extern __shared__ __align__(16) unsigned char fsm[];
-    cx* const buf = reinterpret_cast<cx*>(fsm);  // 2 x (L + L/16) (padded)
-    cx* const bufB = buf + (L + L / 16);
-    float* const Hs = reinterpret_cast<float*>(bufB + (L + L / 16));  // L/2 + 1 (2052 slots)
+    cx* const buf = reinterpret_cast<cx*>(fsm);  // the two exchange buffers (padded)
+    cx* const bufB = buf + kXBuf;
+    float* const Hs = reinterpret_cast<float*>(bufB + kXBuf);  // L/2 + 1 (2052 slots)
     float* const stage = Hs + 2052;                                    // ROWS rows of SLOT_F
     uint64_t* const sbar = reinterpret_cast<uint64_t*>(stage + 2 * kF4kStage);  // staging barrier
     uint32_t* const tslot = reinterpret_cast<uint32_t*>(sbar + 1);             // TMEM address
@@ -599,7 +606,17 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
         fft4096(u, buf, bufB, tmw, i);  // buf's last reader was before bufB's barrier
         // Q = conj(Z): real -> row A, -imag -> row B of each slot, samples 0..Nu-1 (to every
         // destination band that holds the row when scattering).
-        if (p.n_dest == 0) {
+        if (p.n_dest == 0 && p.Nu == SLOT_F && r0 + ROWS <= p.n_rows_total) {
+            // whole group of full-width rows (configs 2-4): row stride SLOT_F, no masks
+            float* const q0 = p.out + r0 * SLOT_F + i;
+#pragma unroll
+            for (int sl = 0; sl < R; ++sl)
+#pragma unroll
+                for (int jj = 0; jj < SJ / 2; ++jj) {
+                    q0[(2 * sl) * SLOT_F + jj * T] = re_(u[sl * SJ + jj]);
+                    q0[(2 * sl + 1) * SLOT_F + jj * T] = -im_(u[sl * SJ + jj]);
+                }
+        } else if (p.n_dest == 0) {
 #pragma unroll
             for (int sl = 0; sl < R; ++sl) {
                 const long rA = r0 + 2 * sl;
