@@ -12,6 +12,7 @@
 // a shared-memory Stockham autosort FFT (one radix-2 pass when log2 L is odd, then radix-4
 // passes), ping-ponging between two L-element complex buffers.  The roofline is HBM:
 // 8 algorithmic bytes per detector pixel (read E, write Q).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -394,58 +395,97 @@ __device__ __forceinline__ void apply_twiddles(cx (&u)[16], const cx (&w)[16])
     for (int j = 1; j < 16; ++j) u[j] = cmulf(u[j], w[j - 1]);
 }
 
-// The two exchanges of a transform go through buffers in natural order with one pad value per
-// 16 (q -> q + q / 16; 64-bit complex values, 32 banks of 4 B; a 64-bit access is served per
-// half-warp).  The span-1 pass of thread i writes X1[16 i + m] at 17 i + m, the span-16 pass of
-// thread i (h = i / 16, k = i mod 16) writes q = 256 h + k + 16 m at 272 h + k + 17 m, and both
-// later passes read x[i + 256 j] at i + i / 16 + 272 j: every half-warp covers the 32 banks
-// once.  (Measured alternatives, r2z: two pads per 16 with the span-1 outputs as 128-bit
-// stores -- the u pairs are not allocated as aligned quads, so every store cost four moves;
-// and a transposed second buffer read as 128-bit loads, which puts a 2-way conflict on the
-// span-16 stores: 4.28 vs 4.01 ms per 256 config-4 views.)
-constexpr int kXBuf = 4096 + 256;  // complex slots per exchange buffer
+// The length-4096 transform as 16 x 256 (n = n1 + 256 n2, k = k1 + 16 k2; thread i, half-warp
+// h = i / 16, lane l = i mod 16):
+//   X[k1 + 16 k2] = sum_n1 w256^(n1 k2) w^(n1 k1) [sum_n2 w16^(n2 k1) x[n1 + 256 n2]].
+// S1: thread i = n1 takes the 16-point DFT over n2 of x[i + 256 n2] (its own registers) and the
+// twiddles w^(i k1).  One CTA exchange (the buffer A: 16 rows k1 of 272 slots) hands row k1 to
+// half-warp h = k1, lane l taking n1 = l + 16 b.  S3: the 256-point DFT of each row inside its
+// half-warp, itself 16 x 16 -- a DFT over b, the twiddles w256^(l c) = w^(16 l c), a warp-local
+// exchange through the half-warp's own row of A (slot 17 c + l, padded) and a DFT over l --
+// leaves lane l = c holding X[h + 16 l + 256 d], d = 0..15.  The inverse is the same algorithm
+// run backwards (the transpose of a DFT is itself, every stage is a block of symmetric DFT16s or
+// a diagonal of twiddles), so it uses the same two twiddle sets and starts from exactly that
+// spectral distribution and ends with thread i holding z[i + 256 n2] -- the input layout -- with
+// the conj trick IDFT(Y) = conj(DFT(conj Y)).  Per transform: one CTA barrier and one warp
+// barrier (Round 2's Stockham form needed two CTA exchanges and two buffers); the row of A a
+// half-warp uses for its warp exchange is the row only it reads, so one 34 KB buffer serves
+// both exchanges of both transforms, and three CTAs fit on an SM.  Bank conflicts: none (the
+// CTA exchange moves consecutive slots per half-warp, the warp exchange has stride 17).
+constexpr int kRow = 272;        // slots per row of A (256 + the 16 x 17 warp exchange)
+constexpr int kXBuf = 16 * kRow;  // complex slots of A
 
-// Full forward transform of u (thread i holds x[i + 256 j]); on return thread i holds
-// X[i + 256 m].  Three radix-16 Stockham passes of spans 1, 16, 256 (decimation in time: pass
-// of span P twiddles its inputs by w^(j P k'), k' = i mod P, then takes a 16-point DFT).  The
-// two exchanges go through two different buffers, so each needs one barrier: a buffer is
-// rewritten only after the barrier that follows its last read.  tw: this thread's
-// tensor-memory twiddle columns.
-template <bool HALF = false>  // HALF: x[i + 256 j] = 0 for j >= 8 (a zero-padded 2048-sample row)
-__device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, uint32_t tw, int i)
+// S1 + twiddles + the write of the CTA exchange.  HALF: x[i + 256 j] = 0 for j >= 8.
+template <bool HALF>
+__device__ __forceinline__ void fwd_s1(cx (&u)[16], cx* A, uint32_t tw, int i)
 {
-    dft16<HALF>(u);  // span 1
-    {
-        cx* const o = buf0 + 17 * i;
+    dft16<HALF>(u);
+    cx w[16];
+    tm_ld32(tw + 32, w);  // w^(j i)
+    tm_wait_ld();
+    apply_twiddles(u, w);
 #pragma unroll
-        for (int m = 0; m < 16; ++m) o[m] = u[m];
-    }
-    __syncthreads();
+    for (int k1 = 0; k1 < 16; ++k1) A[k1 * kRow + i] = u[k1];
+}
+
+// After the CTA barrier: S3 on row h.  Returns X[h + 16 l + 256 d] in u[d].
+__device__ __forceinline__ void fwd_s3(cx (&u)[16], cx* A, uint32_t tw, int i)
+{
+    const int h = i >> 4, l = i & 15;
+    cx* const row = A + h * kRow;
+#pragma unroll
+    for (int b = 0; b < 16; ++b) u[b] = row[l + 16 * b];
+    dft16(u);  // over b -> c
     {
         cx w[16];
-        tm_ld32(tw, w);  // span-16 twiddles, in flight during the exchange's loads
-        const cx* const in = buf0 + i + (i >> 4);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) u[j] = in[272 * j];
+        tm_ld32(tw, w);  // w^(16 l j)
         tm_wait_ld();
         apply_twiddles(u, w);
     }
-    dft16(u);  // span 16
-    {
-        cx* const o = buf1 + 272 * (i >> 4) + (i & 15);
+    __syncwarp();  // the half-warp's reads of its row are done
 #pragma unroll
-        for (int m = 0; m < 16; ++m) o[17 * m] = u[m];
-    }
-    __syncthreads();
+    for (int c = 0; c < 16; ++c) row[17 * c + l] = u[c];
+    __syncwarp();
+#pragma unroll
+    for (int ll = 0; ll < 16; ++ll) u[ll] = row[17 * l + ll];
+    dft16(u);  // over l -> d
+}
+
+// The inverse's S3 backwards from the spectral distribution, then the write of its CTA
+// exchange (row h, n1 = l + 16 b).
+__device__ __forceinline__ void inv_s3(cx (&u)[16], cx* A, uint32_t tw, int i)
+{
+    const int h = i >> 4, l = i & 15;
+    cx* const row = A + h * kRow;
+    dft16(u);  // over d -> l'
     {
         cx w[16];
-        tm_ld32(tw + 32, w);  // span 256: k = i, outputs at i + 256 m stay in this thread
-        const cx* const in = buf1 + i + (i >> 4);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) u[j] = in[272 * j];
+        tm_ld32(tw, w);  // w^(16 l j)
         tm_wait_ld();
         apply_twiddles(u, w);
     }
+    __syncwarp();  // the forward's warp-exchange reads of this row are done
+#pragma unroll
+    for (int ll = 0; ll < 16; ++ll) row[17 * l + ll] = u[ll];
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) u[c] = row[17 * c + l];
+    dft16(u);  // over c -> b
+    __syncwarp();  // the warp-exchange reads of this row are done
+#pragma unroll
+    for (int b = 0; b < 16; ++b) row[l + 16 * b] = u[b];
+}
+
+// After the CTA barrier: thread i = n1 gathers its 16 k1 values, twiddles, DFT over k1.
+// Returns z[i + 256 n2] in u[n2] (before the final conj).
+__device__ __forceinline__ void inv_s1(cx (&u)[16], const cx* A, uint32_t tw, int i)
+{
+    cx w[16];
+    tm_ld32(tw + 32, w);  // w^(j i)
+#pragma unroll
+    for (int k1 = 0; k1 < 16; ++k1) u[k1] = A[k1 * kRow + i];
+    tm_wait_ld();
+    apply_twiddles(u, w);
     dft16(u);
 }
 
@@ -457,7 +497,7 @@ __device__ __forceinline__ void fft4096(cx (&u)[16], cx* buf0, cx* buf1, uint32_
 // zeroed once per launch: a copy writes the first N_u floats of a slot, so the padding after
 // them stays zero and the rows are read without masks.
 constexpr int kF4kStage = 2048;  // floats per staged row (Nu <= 2048)
-constexpr size_t kF4kSmem = 2 * sizeof(float2) * f4k::kXBuf + sizeof(float) * 2052 +
+constexpr size_t kF4kSmem = sizeof(float2) * f4k::kXBuf + sizeof(float) * 4096 +
                             sizeof(float) * 2 * kF4kStage + 16;
 
 // Destination row of view t, detector row v in band d, or nullptr if v is outside the band.
@@ -474,7 +514,7 @@ __device__ __forceinline__ float* dest_row_tv(const FilterParams& p, long t, int
 // and each slot's first N_u outputs are exactly that row's linear convolution.  Configs 2 / 3
 // (N_u = 512 / 1024) run 4 / 2 row pairs per transform.
 template <bool ASYNC, int R>
-__global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p,
+__global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p,
                                                             const float2* __restrict__ tw_g,
                                                             const float* __restrict__ Hs_g)
 {
@@ -483,10 +523,9 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
     constexpr int ROWS = 2 * R;         // rows per transform
     constexpr int SLOT_F = 4096 / ROWS; // staged floats per row (>= N_u)
     extern __shared__ __align__(16) unsigned char fsm[];
-    cx* const buf = reinterpret_cast<cx*>(fsm);  // the two exchange buffers (padded)
-    cx* const bufB = buf + kXBuf;
-    float* const Hs = reinterpret_cast<float*>(bufB + kXBuf);  // L/2 + 1 (2052 slots)
-    float* const stage = Hs + 2052;                                    // ROWS rows of SLOT_F
+    cx* const A = reinterpret_cast<cx*>(fsm);                  // the exchange buffer
+    float* const Hp = reinterpret_cast<float*>(A + kXBuf);      // H in spectral order
+    float* const stage = Hp + 4096;                             // ROWS rows of SLOT_F
     uint64_t* const sbar = reinterpret_cast<uint64_t*>(stage + 2 * kF4kStage);  // staging barrier
     uint32_t* const tslot = reinterpret_cast<uint32_t*>(sbar + 1);             // TMEM address
     const int i = threadIdx.x, warp = i >> 5;
@@ -496,7 +535,13 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int f = i; f <= L / 2; f += T) Hs[f] = Hs_g[f];
+    // Hp[256 d + i'] = H[f], f = h' + 16 l' + 256 d (h' = i' / 16, l' = i' mod 16): the
+    // frequency thread i' holds in u[d] after the forward transform (H real and even:
+    // H[f] = H[L - f] past L / 2), read without bank conflicts.
+    for (int e = i; e < L; e += T) {
+        const int ii = e & 255, f = (ii >> 4) + 16 * (ii & 15) + (e & ~255);
+        Hp[e] = Hs_g[f <= L / 2 ? f : L - f];
+    }
     if (ASYNC)
         for (int e = i; e < 2 * kF4kStage; e += T) stage[e] = 0.f;
     const long n_groups = (p.n_rows_total + ROWS - 1) / ROWS;
@@ -588,22 +633,19 @@ __global__ void __launch_bounds__(256, 2) filter_f4k_kernel(const FilterParams p
             const cx q = cfma2(mk(uh, uh), mk(uh, uh), mk(dA[sl], dB[sl]));
             u[j] = cmul2(mk(ea, eb), mk(rsqrt_ftz(re_(q)), rsqrt_ftz(im_(q))));
         }
-        __syncthreads();  // staging read and buffers free: fetch the next group meanwhile
+        fwd_s1<R == 1>(u, A, tmw, i);
+        __syncthreads();  // exchange written, staging read out: fetch the next group meanwhile
         prefetch(gi + gridDim.x);
-        fft4096<R == 1>(u, buf, bufB, tmw, i);
+        fwd_s3(u, A, tmw, i);
         // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
-        // X[f], f = i + 256 m, takes H[f] for m < 8 and H[L - f] for m >= 8 (f = L/2 only for
-        // m = 8, i = 0, where both are H[L/2]).
-        {
-            const float* hp = Hs + i;
-            const float* hn = Hs + (L - i);
 #pragma unroll
-            for (int m = 0; m < 16; ++m) {
-                const float h = m < 8 ? hp[256 * m] : hn[-256 * m];
-                u[m] = cmul2(u[m], mk(h, -h));
-            }
+        for (int d = 0; d < 16; ++d) {
+            const float h = Hp[256 * d + i];
+            u[d] = cmul2(u[d], mk(h, -h));
         }
-        fft4096(u, buf, bufB, tmw, i);  // buf's last reader was before bufB's barrier
+        inv_s3(u, A, tmw, i);
+        __syncthreads();
+        inv_s1(u, A, tmw, i);
         // Q = conj(Z): real -> row A, -imag -> row B of each slot, samples 0..Nu-1 (to every
         // destination band that holds the row when scattering).
         if (p.n_dest == 0 && p.Nu == SLOT_F && r0 + ROWS <= p.n_rows_total) {
@@ -746,8 +788,6 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
         int R = 1;
         while (R < 8 && 4096 / (2 * R) >= 2 * g->Nu - 1) R *= 2;
         const long groups = (total + 2 * R - 1) / (2 * R);
-        long grid = (long)sms * 2;  // persistent: the resident CTAs per SM
-        if (grid > groups) grid = groups;
         // In-place filtering is safe with the prefetch: a group's rows are fetched before any
         // CTA writes them (each group belongs to one CTA) and never read again.  (A scatter
         // destination must not alias the raw views.)
@@ -760,6 +800,23 @@ ifdk_status launch_filter(ifdk_geometry* g, const float* raw, float* out, long n
                      : pick(filter_f4k_kernel<true, 1>, filter_f4k_kernel<false, 1>);
         e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4kSmem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter)");
+        // persistent grid: the CTAs that fit on an SM by registers and shared memory (3 for the
+        // 68 KB, <= 80-register kernel; 128 tensor-memory columns each, at most 4 per SM).
+        // (cudaOccupancyMaxActiveBlocksPerMultiprocessor answered 1 for this kernel.)
+        e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(filter carveout)");
+        cudaFuncAttributes fa;
+        if ((e = cudaFuncGetAttributes(&fa, k)) != cudaSuccess)
+            return cuda_fail(e, "cudaFuncGetAttributes(filter)");
+        int sm_smem = 0, reserved = 0;
+        cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        const int regs = (fa.numRegs + 7) / 8 * 8;
+        int per_sm = 4;
+        per_sm = std::min(per_sm, 65536 / (regs * 256));
+        per_sm = std::min(per_sm, sm_smem / (int)(kF4kSmem + reserved));
+        long grid = (long)sms * (per_sm > 0 ? per_sm : 1);
+        if (grid > groups) grid = groups;
         k<<<(unsigned)grid, 256, kF4kSmem, st>>>(p, g->dev[dev].tw, g->dev[dev].Hs);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "filter_f4k_kernel launch");
