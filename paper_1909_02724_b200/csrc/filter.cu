@@ -349,22 +349,25 @@ __device__ __forceinline__ void dft16(cx (&u)[16])
 // costs one tcgen05.ld of 32 registers (issued before the exchange's shared loads, awaited
 // after them) and 15 complex multiplies.  (Round 2's first form read four power tables per
 // pass and composed the other eleven powers: 22 % of the kernel's instructions, r2x capture.)
-__device__ __forceinline__ void tm_ld32(uint32_t taddr, cx (&w)[16])
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, cx* w)  // w[0..7] = columns 0..15
 {
-    uint32_t r[32];
+    uint32_t r[16];
     asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-        "%28, %29, %30, %31}, [%32];"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15}, [%16];"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
           "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-          "=r"(r[31])
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
         : "r"(taddr));
 #pragma unroll
-    for (int m = 0; m < 16; ++m) w[m] = mk(__uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
+    for (int m = 0; m < 8; ++m) w[m] = mk(__uint_as_float(r[2 * m]), __uint_as_float(r[2 * m + 1]));
+}
+// Two 16-column loads rather than one of 32: a 32-register destination block made ptxas move
+// the live transform values out of its way (about 30 moves per row group, r2z6 capture).
+__device__ __forceinline__ void tm_ld32(uint32_t taddr, cx (&w)[16])
+{
+    tm_ld16(taddr, w);
+    tm_ld16(taddr + 16, w + 8);
 }
 
 __device__ __forceinline__ void tm_st32(uint32_t taddr, const cx (&w)[16])
@@ -566,7 +569,7 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
         tm_wait_st();
     }
     auto prefetch = [&](long gi) {  // one thread: the group's rows by 1-D bulk copies
-        if (!ASYNC || gi >= n_groups || i != 0) return;
+        if (!ASYNC || i != 0 || gi >= n_groups) return;
         const long r0 = ROWS * gi;
         const int nrow = (int)min((long)ROWS, p.n_rows_total - r0);
         // a partial last group: the missing rows' slots are zeroed (they share the transforms)
@@ -586,6 +589,7 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
     long t0 = (long)ROWS * blockIdx.x / nr;
     int vr0 = (int)((long)ROWS * blockIdx.x - t0 * nr);
     uint32_t sphase = 0;
+    const float uh0 = ((float)i - p.cu) * p.Du;  // uh of sample n = i + 256 jj: uh0 + 256 jj Du
     for (long gi = blockIdx.x; gi < n_groups; gi += gridDim.x) {
         const long r0 = ROWS * gi;
         // D^2 + vh^2 of rows A = r0 + 2 s (real part) and B = r0 + 2 s + 1 (imaginary part)
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
                     if (rB < p.n_rows_total) eb = __ldg(p.raw + rB * p.Nu + n);
                 }
             }
-            const float uh = ((float)n - p.cu) * p.Du;
+            const float uh = fmaf((float)(jj * T), p.Du, uh0);
             const cx q = cfma2(mk(uh, uh), mk(uh, uh), mk(dA[sl], dB[sl]));
             u[j] = cmul2(mk(ea, eb), mk(rsqrt_ftz(re_(q)), rsqrt_ftz(im_(q))));
         }
