@@ -165,20 +165,20 @@ def ncu_field(config: int, key: str):
 
 
 def walk_smem_bytes(spec):
-    """Algorithmic shared-memory bytes per update of the k-walk the library picks for the
-    geometry: per 64-slice chunk and view a thread issues LDS.32 taps --
-    4-row TRIPLE (0.5 <= dv/dk): ten 3+3-slice groups x 16 taps + a 4-slice PAIR quad x 12 taps
-    = 688 B / 64 updates = 10.75 B; 3-row TRIPLE (dv/dk < 0.5): 10 x 12 + 12 taps = 8.25 B;
-    PAIR: 12 taps per 4 updates = 12 B."""
+    """Algorithmic shared-memory bytes per update and kernel of the k-walk the library picks
+    for the geometry: per 64-slice chunk and view a thread issues LDS.32
+    taps -- QUAD (0.5 <= dv/dk < 1): eight 4+4-slice groups x 20 taps = 640 B / 64 updates =
+    10 B; 3-row TRIPLE (dv/dk < 0.5): ten 3+3-slice groups x 12 + a PAIR quad x 12 taps =
+    8.25 B; PAIR: 12 taps per 4 updates = 12 B."""
     import math
 
     r = math.hypot(spec.Nx * spec.Dx, spec.Ny * spec.Dy) / 2
     dv = [spec.D / spec.Dv * spec.Dz / z for z in (spec.d + r, spec.d - r)]
-    if min(dv) >= 0.5001:
-        return 10.75, "4-row TRIPLE"
+    if min(dv) >= 0.5001 and max(dv) < 0.9999:
+        return 10.0, "QUAD", "bp_quad2_kernel"
     if max(dv) < 0.4999:
-        return 8.25, "3-row TRIPLE"
-    return 12.0, "PAIR"
+        return 8.25, "3-row TRIPLE", "bp_tmem2_kernel"
+    return 12.0, "PAIR", "bp_raw_kernel"
 
 
 def smem_probe():
@@ -444,7 +444,7 @@ def run_ours(args, spec, rank, world, local_rank):
         bp_s = stage.get("bp_ms", float("nan")) / 1e3 / max(plan.n_rounds, 1)
         upd_per_launch = spec.Nx * spec.Ny * nk * spec.Np / max(plan.n_rounds, 1)
         bp_share = stage.get("bp_ms", float("nan")) / ms
-    walk_b, walk_name = walk_smem_bytes(spec)
+    walk_b, walk_name, bp_kernel = walk_smem_bytes(spec)
     achieved_gbs = walk_b * upd_per_launch / bp_s / 1e9
     achieved_4tap_gbs = SMEM_BYTES_PER_UPDATE * upd_per_launch / bp_s / 1e9
     hbm_peak = float(measured_peaks().get("hbm_gbs", 6543.4))
@@ -455,7 +455,7 @@ def run_ours(args, spec, rank, world, local_rank):
     bp_hbm_bytes = 4 * views_per_launch * spec.Nu * spec.Nv + 8 * spec.Nx * spec.Ny * nk
     roofline_hbm = {"bound": "hbm", "achieved": bp_hbm_bytes / bp_s / 1e9, "peak": hbm_peak,
                     "unit": "GB/s", "frac": bp_hbm_bytes / bp_s / 1e9 / hbm_peak,
-                    "kernel": "bp_tmem2_kernel (4 B per filtered pixel + 8 B per voxel per launch)",
+                    "kernel": f"{bp_kernel} (4 B per filtered pixel + 8 B per voxel per launch)",
                     "peak_basis": "MEASURED_PEAKS.json hbm_gbs"}
     # BP against the issue roofline: SASS instructions per update from the committed ncu
     # capture (profiles/ncu_bp_traffic.json "inst_per_update") x updates/s, against
@@ -469,7 +469,7 @@ def run_ours(args, spec, rank, world, local_rank):
         roofline_issue = {"bound": "issue", "achieved": ach_ti, "peak": peak_ti,
                           "unit": "Tinst/s (thread)", "frac": ach_ti / peak_ti,
                           "inst_per_update": ipu,
-                          "kernel": "bp_tmem2_kernel",
+                          "kernel": bp_kernel,
                           "peak_basis": "148 SM x 4 x 32 x sm_max_mhz; inst_per_update from the "
                                         "committed ncu capture (profiles/ncu_bp_traffic.json)"}
     filt = None
@@ -833,7 +833,7 @@ def run_ours(args, spec, rank, world, local_rank):
                                  / (256.0 * spec.Nx * spec.Ny * spec.Nz)
                                  if ncu_traffic(args.config) else None),
                      "bytes_per_update": walk_b,
-                     "kernel": f"bp_tmem2_kernel ({walk_name} walk: {walk_b} algorithmic B/update "
+                     "kernel": f"{bp_kernel} ({walk_name} walk: {walk_b} algorithmic B/update "
                                "of shared-memory taps; TMEM accumulators, two views per step)",
                      "smem_bytes_per_update_ncu": ncu_field(args.config, "smem_bytes_per_update"),
                      "four_tap": {"bytes_per_update": SMEM_BYTES_PER_UPDATE,

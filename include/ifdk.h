@@ -290,12 +290,15 @@ ifdk_status ifdk_mlem_update(float* x_dev, const float* c_dev, const float* C_de
 ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream);
 
 /* Speed-tuning hook for A/B measurements and tests, not needed in normal use:
- * walk selects the back-projection k-walk among the variants that give BITWISE
- * the same result as the automatic choice for the geometry (PAIR family 2, 4, 5;
- * 4-row TRIPLE family 3, 6, 9, 11 where 0.5 <= dv/dk; 3-row TRIPLE family 7, 8,
- * 10, 12 where dv/dk < 0.5; 9-12 keep the accumulators in tensor memory, 11 / 12
- * step two views at a time); any other value, or 0, means
- * automatic.
+ * walk selects the back-projection k-walk; within a family the variants give
+ * BITWISE the same result (PAIR family 2, 4, 5; 4-row TRIPLE family 3, 6, 9, 11
+ * where 0.5 <= dv/dk; 3-row TRIPLE family 7, 8, 10, 12 where dv/dk < 0.5; 9-12
+ * keep the accumulators in tensor memory, 11 / 12 step two views at a time), and
+ * the QUAD walk 13 (the automatic choice where 0.5 <= dv/dk < 1: four slices per
+ * floor, tensor-memory accumulators, two views per step, partial chunks in the
+ * same kernel) is its own family -- it agrees with the others to fp32 rounding,
+ * not bitwise.  A walk outside the geometry's range, or 0,
+ * means automatic.
  * raster sets the CTA raster band in tiles (0 = automatic; >= the tile count =
  * row-major); it only reorders CTAs.  Process-wide; affects later launches. */
 ifdk_status ifdk_set_bp_variant(int walk, int raster);

@@ -117,6 +117,12 @@ struct __align__(16) Meta {
     int u_org, v_org;    // box origin (detector column, row)
     int w_need, h_need;  // columns / rows of the box the tile x chunk can touch
     int fast;            // the patch fits the box
+    // QUAD walk (WALK 13): the tile corner's invariants in fp64, split (u_c = uci + ucf,
+    // v_c(kb) = vci + vcf), the corner's u_c, v_c, z_c rounded to fp32 and the used entries of
+    // P_s rounded to fp32 -- each thread adds its small offset from the corner in fp32
+    int uci, vci;
+    float ucf, vcf, uc, vc, zc;
+    float p0, p1, p3, p4, p5, p7, p8;
     int pad[3];
 };
 
@@ -572,6 +578,18 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
         vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
+    if (WALK == 13 && lane == 0) {  // lane 0 holds the tile corner (i_corner, j_corner) = base
+        const double fu = floor(c.u), fv = floor(c.v);
+        m->uci = (int)fu;
+        m->vci = (int)fv;
+        m->ucf = (float)(c.u - fu);
+        m->vcf = (float)(c.v - fv);
+        m->uc = (float)c.u;
+        m->vc = (float)c.v;
+        m->zc = (float)(1.0 / c.f);
+        m->p0 = (float)P[0]; m->p1 = (float)P[1]; m->p3 = (float)P[3]; m->p4 = (float)P[4];
+        m->p5 = (float)P[5]; m->p7 = (float)P[7]; m->p8 = (float)P[8];
+    }
     if (lane == 0) {
         const double fu0 = floor(umin), fu1 = floor(umax), fv0 = floor(vmin), fv1 = floor(vmax);
         // TMA (tile mode, no swizzle) faults unless the innermost box coordinate is a
@@ -579,10 +597,12 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
         // rounded down to a multiple of 4 floats.
         const bool finite = fu0 > -1e9 && fu1 < 1e9 && fv0 > -1e9 && fv1 < 1e9;
         const int u_org = finite ? (((int)fu0 - 1) & ~3) : 0;
-        const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0 + p.pair;
+        // QUAD: one more row below (its fp32 thread floors may sit one below the corners')
+        constexpr int MV = WALK == 13 ? 1 : 0;
+        const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0 + p.pair + MV;
         const bool fits = finite && w_need <= p.box_w && h_need <= p.box_h;
         m->u_org = u_org;
-        m->v_org = finite ? (int)fv0 - 1 : 0;
+        m->v_org = finite ? (int)fv0 - 1 - MV : 0;
         m->fast = fits ? 1 : 0;
         m->w_need = fits ? (int)w_need : 0;
         m->h_need = fits ? (int)h_need : 0;
@@ -1604,6 +1624,264 @@ __global__ void __launch_bounds__(kThreads, 3)
                      : "memory");
 }
 
+// ---------------------------------------------------------------------------------------------
+// QUAD walk (walk 13, the default where 0.5 <= dv/dk < 1, configs 1-4): runs of four slices
+// around a base slice b whose floor n = floor(v_b) serves all four.  Slice b + j sits at
+// p = f_v + j dv from row n; for j = -1, 0, 1, 2 it lies within one row of row n + r_j
+// (r = 0, 0, 1, 2): g_j = p - r_j is in [-1, 1) exactly when 0.5 <= dv <= 1 (the TRIPLE
+// walk's condition), so every slice is Alg. alg:subpixel on the pair of rows around n + r_j,
+// written from that row (h + g (g >= 0 ? h+ - h : h - h-)).  Five rows n-1 .. n+3 feed four
+// slices: 10 LDS.32 per 4 updates and half, 2.5 per update (TRIPLE 2.67, PAIR 3), and 30 FP32x2
+// + 12 selects + 2 IMAD per 8 updates (TRIPLE: 50 instructions per 6).  The walk is bounded by
+// shared-memory wavefronts (LSU pipe 71 % for TRIPLE, r2x capture), so the 6 % fewer
+// wavefronts and 4 % fewer instructions go straight to the rate.  The two FP32x2 halves carry
+// the runs b = 8q + 1 (slices 8q .. 8q+3) and 8q + 5 (8q+4 .. 8q+7): eight groups tile the
+// 64-slice chunk with no tail.  Row n-1 stays inside the staged box (its origin is
+// floor(v_min) - 1, compute_meta1), row n+3 too (floor(v_63) + 2 >= floor(v_61) + 3).
+// Partial chunks (slab ends inside a chunk) run the same walk over all 64 slices with the box of
+// the whole chunk and write back only the slab's slices, so every slab split is bitwise one
+// launch without a companion walk.
+// The QUAD kernel's per-(column, view) invariants in fp32 from the tile corner's fp64 values
+// (Meta, compute_meta1<.., 13>): with the column's offsets di, dj < 16 from the corner,
+// x = x_c + dx, z = z_c + dz and u = x / z = u_c + (dx - u_c dz) / z, the correction a few
+// pixels in size, so its fp32 rounding (~1e-6 px) stays far below the tolerance while x = u z
+// itself (~1e6) would cancel (SURVEY c-N1).  Same for v(kb).  About 20 fp32 instructions per
+// view instead of 7 DFMA, an fp64 reciprocal, 4 DMUL and 8 conversions (round 2: the per-view
+// invariants were a fifth of the two-view step's instructions).
+__device__ __forceinline__ float rcp_approx(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ ThreadInv quad_inv(const Meta& m, float fdi, float fdj)
+{
+    ThreadInv t;
+    const float dx = fmaf(m.p0, fdi, m.p1 * fdj);
+    const float dy = fmaf(m.p3, fdi, m.p4 * fdj);
+    const float dz = fmaf(m.p7, fdi, m.p8 * fdj);
+    const float f = rcp_approx(m.zc + dz);
+    const f2x s2 = pk2(fmaf(fmaf(-m.uc, dz, dx), f, m.ucf), fmaf(fmaf(-m.vc, dz, dy), f, m.vcf));
+    // floor by the round-down magic add of 1.5 * 2^23 (|s| < 2^22): bits - 0x4B400000 = floor(s)
+    const f2x t2 = add2_rd(s2, pk2(12582912.0f, 12582912.0f));
+    const f2x fr = sub2(s2, add2(t2, pk2(-12582912.0f, -12582912.0f)));
+    t.nu = m.uci + (int)(__float_as_uint(lo2(t2)) - 0x4B400000u);
+    t.nv = m.vci + (int)(__float_as_uint(hi2(t2)) - 0x4B400000u);
+    t.du = lo2(fr);
+    t.fv0 = hi2(fr);
+    t.dv = m.p5 * f;
+    t.dvm1 = t.dv - 1.f;
+    t.W = f * f;
+    return t;
+}
+
+template <int BW, int Q0, int NQ>
+__device__ __forceinline__ void quad_groups(f2x (&acc)[4 * NQ], uint32_t a0, const ThreadInv& t)
+{
+    constexpr uint32_t S = BW * 4;
+    const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
+    const f2x du2 = pk2(t.du, t.du);
+    const f2x magic2 = pk2(8388608.0f, 8388608.0f), nmagic2 = pk2(-8388608.0f, -8388608.0f);
+    const f2x fv02 = pk2(t.fv0, t.fv0);
+    f2x kvec = pk2((float)(8 * Q0 + 1), (float)(8 * Q0 + 5));  // the two runs' base slices
+    asm volatile("mov.b64 %0, %0;" : "+l"(kvec));
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+        const f2x v = fma2(kvec, dv2, fv02);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(kvec) : "l"(pk2(8.f, 8.f)));
+        const f2x tb = add2_rd(v, magic2);
+        const f2x fr = sub2(v, add2(tb, nmagic2));
+        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        f2x h[5];  // rows n-1 .. n+3
+#pragma unroll
+        for (int r = 0; r < 5; ++r) {
+            const f2x a = pk2(lds32(adA + (r - 1) * S), lds32(adB + (r - 1) * S));
+            const f2x b = pk2(lds32(adA + (r - 1) * S + 4), lds32(adB + (r - 1) * S + 4));
+            h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
+        }
+        f2x d[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) d[r] = sub2(h[r + 1], h[r]);
+        const f2x gm = sub2(fr, dv2);       // slice b - 1 from row n
+        const f2x g1 = add2(fr, dvm12);     // slice b + 1 from row n + 1
+        const f2x g2 = add2(g1, dvm12);     // slice b + 2 from row n + 2
+        acc[4 * qq] = fma2(W2, fma2(gm, sel2(d[1], d[0], gm), h[1]), acc[4 * qq]);  // line 6;
+        acc[4 * qq + 1] = fma2(W2, fma2(fr, d[1], h[1]), acc[4 * qq + 1]);         // Alg. alg:bp
+        acc[4 * qq + 2] = fma2(W2, fma2(g1, sel2(d[2], d[1], g1), h[2]), acc[4 * qq + 2]);
+        acc[4 * qq + 3] = fma2(W2, fma2(g2, sel2(d[3], d[2], g2), h[3]), acc[4 * qq + 3]);
+    }
+}
+
+// Two groups (16 TMEM columns: pair 4 q + m = slices 8 q + m / 8 q + 4 + m) of two views.
+template <int BW, int Q0>
+__device__ __forceinline__ void quad_sub2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
+                                          uint32_t a1, const ThreadInv& u)
+{
+    f2x acc[8];
+    tm_ld16(tacc + 8 * Q0, acc);
+    tm_wait_ld();
+    quad_groups<BW, Q0, 2>(acc, a0, t);
+    quad_groups<BW, Q0, 2>(acc, a1, u);
+    tm_st16(tacc + 8 * Q0, acc);
+}
+
+template <int BW>
+__device__ __forceinline__ void walk_views_quad2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
+                                                 uint32_t a1, const ThreadInv& u)
+{
+    tm_wait_st();
+    quad_sub2<BW, 0>(tacc, a0, t, a1, u);
+    quad_sub2<BW, 2>(tacc, a0, t, a1, u);
+    quad_sub2<BW, 4>(tacc, a0, t, a1, u);
+    quad_sub2<BW, 6>(tacc, a0, t, a1, u);
+}
+
+// Flush of the QUAD accumulators: slices of the slab only (a partial chunk's other slices
+// were walked but are not written), zeros back.
+template <bool RED>
+__device__ __forceinline__ void flush_quad(uint32_t tacc, const BPParams& p, int i, int j, int kb,
+                                           bool overwrite, bool inside)
+{
+    tm_wait_st();
+    float* q0 = vol_voxel(p, kb, j, i);
+    const long plane = (long)p.Ny * p.Nx;
+    const int klo = p.k0 - kb, khi = p.k0 + p.nk - kb;  // slab slices of this chunk: [klo, khi)
+    const f2x zero[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int part = 0; part < 4; ++part) {  // pairs 8 part .. 8 part + 7
+        f2x a[8];
+        tm_ld16(tacc + 16 * part, a);
+        tm_wait_ld();
+        if (inside) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int pi = 8 * part + m;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const int kk = 8 * (pi / 4) + 4 * half + pi % 4;
+                    const float v = half ? hi2(a[m]) : lo2(a[m]);
+                    if (kk >= klo && kk < khi)
+                        put_voxel<RED>(p, q0 + kk * plane, kb + kk, j, i, v, overwrite);
+                }
+            }
+        }
+        tm_st16(tacc + 16 * part, zero);
+    }
+}
+
+// The two-views-per-step TMEM kernel (bp_tmem2_kernel's pipeline) with the QUAD walk; whole and
+// partial chunks alike.
+template <int BW, bool RED = false>
+__global__ void __launch_bounds__(kThreads, 3)
+    bp_quad2_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
+                    const __grid_constant__ PTable pt)
+{
+    constexpr int KC = 64, NB = kRawBuf2, VB = 128;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tile_i = (int)blockIdx.z * p.raster + (int)(blockIdx.x % (unsigned)p.raster);
+    const int tile_j = (int)(blockIdx.x / (unsigned)p.raster);
+    if (tile_i >= p.tiles_i) return;
+    const int i = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+    const int j = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+    const int ic = min(i, p.Nx - 1), jc = min(j, p.Ny - 1);
+    const int i_corner = (lane & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
+    const int j_corner = (lane & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
+    const int kb = p.kb0 + (int)blockIdx.y * KC;
+    if (p.vb != VB) __trap();
+    const int n = (int)p.n_views;
+
+    unsigned char* const raw = smem;
+    Meta* const meta = reinterpret_cast<Meta*>(raw + NB * p.raw_bytes);
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(meta + kMetaRing);
+    uint32_t* const tslot = reinterpret_cast<uint32_t*>(mbar + NB);
+    const uint32_t tx_bytes = (uint32_t)(BW * p.box_h * 4);
+    const CUtensorMap* const tmap_ptr = &tmap;
+    const PTable* const ptab = &pt;
+    const uint32_t raw0 = smem_u32(raw);
+
+    auto issue = [=](int t) {
+        const Meta& m = meta[t & (kMetaRing - 1)];
+        if (!m.fast) __trap();
+        const int b = t % NB;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&mbar[b], tx_bytes);
+        tma_load_3d(raw + b * p.raw_bytes, tmap_ptr, &mbar[b], m.u_org, m.v_org - p.v0, t);
+    };
+    auto metas = [=](int t0) {  // boxes of the whole chunk (partial chunks too)
+        if (t0 + warp < n)
+            compute_meta1<KC, 13>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner,
+                                  kb, 0, KC);
+    };
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                         smem_u32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 0) {
+        for (int b = 0; b < NB; ++b) mbar_init(&mbar[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    metas(0);
+    int meta_next = 8;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tacc = *tslot + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    if (tid == 0)
+        for (int t = 0; t < NB && t < n; ++t) issue(t);
+    {
+        const f2x zero[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+        for (int part = 0; part < 4; ++part) tm_st16(tacc + 16 * part, zero);
+    }
+
+    const int first_flush = (int)(VB - 1 - (p.s0 % VB + VB) % VB);
+    const float fdi = (float)(ic - tile_i * kTI), fdj = (float)(jc - tile_j * kTJ);
+    const uint32_t nm = p.neg_magic;
+    for (int t = 0; t < n;) {
+        const bool two = t + 1 < n && !(t == 0 && (first_flush & 1) == 0);
+        const int te = two ? t + 1 : t;
+        const Meta& m0 = meta[t & (kMetaRing - 1)];
+        const Meta& m1 = meta[te & (kMetaRing - 1)];
+        const ThreadInv ti = quad_inv(m0, fdi, fdj);
+        ThreadInv tu = quad_inv(m1, fdi, fdj);
+        if (!two) tu.W = 0.f;
+        mbar_wait(&mbar[t % NB], (uint32_t)((t / NB) & 1));
+        if (two) mbar_wait(&mbar[te % NB], (uint32_t)((te / NB) & 1));
+        const uint32_t a0 = raw0 + (uint32_t)((t % NB) * p.raw_bytes) +
+                            (uint32_t)(((ti.nv - m0.v_org) * BW + (ti.nu - m0.u_org)) * 4) + nm;
+        const uint32_t a1 = raw0 + (uint32_t)((te % NB) * p.raw_bytes) +
+                            (uint32_t)(((tu.nv - m1.v_org) * BW + (tu.nu - m1.u_org)) * 4) + nm;
+        walk_views_quad2<BW>(tacc, a0, ti, a1, tu);
+        if ((te >= first_flush && ((te - first_flush) & (VB - 1)) == 0) || te == n - 1) {
+            const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
+            const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
+            const bool ow = !p.accumulate && te <= first_flush;
+            flush_quad<RED>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
+        }
+        if (te + NB >= meta_next && meta_next < n) {
+            metas(meta_next);
+            meta_next += 8;
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (int v = t + NB; v <= te + NB; ++v)
+                if (v < n) issue(v);
+        t = te + 1;
+    }
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(*tslot)
+                     : "memory");
+}
+
 // Opt-in dynamic shared memory per CTA of the current device.
 int max_dyn_smem()
 {
@@ -1675,10 +1953,11 @@ int choose_walk(const ifdk_geometry* g)
     if (!use_pair(g)) return 1;
     const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
     const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
-    int w = dv_min >= 0.5001 ? 11 : dv_max < 0.4999 ? 12 : 5;
+    int w = dv_min >= 0.5001 && dv_max < 0.9999 ? 13 : dv_max < 0.4999 ? 12 : 5;
     const int v = g_walk_override.load(std::memory_order_relaxed);
     if (v == 2 || v == 4 || v == 5) w = v;
     if ((v == 3 || v == 6 || v == 9 || v == 11) && dv_min >= 0.5001) w = v;
+    if (v == 13 && dv_min >= 0.5001 && dv_max < 0.9999) w = v;
     if ((v == 7 || v == 8 || v == 10 || v == 12) && dv_max < 0.4999) w = v;
     return w;
 }
@@ -1730,7 +2009,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     double wb, hb;
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     p.pair = use_pair(g) ? 1 : 0;
-    const int walk = KC == 64 ? choose_walk(g) : (p.pair ? 2 : 1);
+    int walk = KC == 64 ? choose_walk(g) : (p.pair ? 2 : 1);
     const int box_h = (int)std::ceil(hb) + 6 + p.pair;
     const int box_w0 = std::max(8, ((int)std::ceil(wb) + 9 + 3) / 4 * 4);  // +3: 16-B origin
     // Raster band of 16 tile columns: measured on B200 (config 4, one 256-view launch) DRAM
@@ -1751,7 +2030,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         int box_w = box_w0, P2 = 0, BW = 0;
         for (int c : {24, 40, 56, 72})
             if (c >= box_w - 1) { P2 = c; break; }
-        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 12)) {
+        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 13)) {
             for (int c : {40, 72})  // row pitch = 8 mod 32 words: conflict-free LDS.32 taps
                 if (c >= box_w) { BW = c; break; }
             box_w = BW;
@@ -1769,7 +2048,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
             };
             // two views per step want six boxes; where those do not fit three CTAs per SM
             // (tall or wide boxes) the one-view step (four boxes) is the faster choice
-            if (w >= 11 && 3 * (raw_smem(kRawBuf2) + 1024) > 228 * 1024) w = w % 2 ? 9 : 10;
+            if (w >= 11 && w <= 12 && 3 * (raw_smem(kRawBuf2) + 1024) > 228 * 1024) w = w % 2 ? 9 : 10;
             const int nbuf = w >= 11 ? kRawBuf2 : kRawBuf;
             smem = BW ? raw_smem(nbuf)
                       : 2 * (size_t)q.raw_bytes + 2 * sizeof(float2) * box_h * P2 +
@@ -1796,6 +2075,18 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         q.neg_magic = 0u - 0x4B000000u * (uint32_t)(BW ? BW * 4 : P2 * 8);
         dim3 grid((unsigned)(q.raster * tiles_j), (unsigned)nch,
                   (unsigned)((q.tiles_i + q.raster - 1) / q.raster));
+        if (BW && w == 13) {
+            auto k = q.red ? (BW == 40 ? bp_quad2_kernel<40, true> : bp_quad2_kernel<72, true>)
+                           : (BW == 40 ? bp_quad2_kernel<40> : bp_quad2_kernel<72>);
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp quad)");
+            k<<<grid, kThreads, smem, st>>>(q, map, pt);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "bp_quad2_kernel launch");
+            count_launch();
+            return IFDK_OK;
+        }
         if (BW && w >= 9 && w <= 12) {
             auto k = w == 9    ? (BW == 40 ? bp_tmem_kernel<40, 1, 3> : bp_tmem_kernel<72, 1, 3>)
                      : w == 10 ? (BW == 40 ? bp_tmem_kernel<40, 2, 3> : bp_tmem_kernel<72, 2, 3>)
@@ -1873,8 +2164,17 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         }
     };
 
-    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 12)) || !tma_ok || box_w0 > 72)
+    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 13)) || !tma_ok || box_w0 > 72)
         return run(walk, p.kb0, n_chunks);
+    if (walk == 13) {
+        // the QUAD kernel walks partial chunks itself (one launch for the slab) when its six
+        // boxes fit three CTAs per SM; otherwise the TRIPLE family (walk 11 + companions)
+        const int bw = box_w0 <= 40 ? 40 : 72;
+        const size_t raw_bytes = ((size_t)bw * box_h * 4 + 127) / 128 * 128;
+        const size_t smem6 = kRawBuf2 * raw_bytes + kMetaRing * sizeof(Meta) + 8 * kRawBuf2 + 16;
+        if (3 * (smem6 + 1024) <= 228 * 1024) return run(13, p.kb0, n_chunks);
+        walk = 11;
+    }
     // RAW staging runs the whole chunks; a partial chunk at either slab end (its masked slices
     // would read rows outside the box) takes the x2 pair walk, bitwise the same values.
     const bool head = (k0 % KC) != 0, tail = ((k0 + nk) % KC) != 0;
@@ -1941,8 +2241,10 @@ void preload_bp_kernels()
     touch_kernel(bp_tmem2_kernel<72, 1, true>);
     touch_kernel(bp_tmem2_kernel<40, 2, true>);
     touch_kernel(bp_tmem2_kernel<72, 2, true>);
-
-
+    touch_kernel(bp_quad2_kernel<40>);
+    touch_kernel(bp_quad2_kernel<72>);
+    touch_kernel(bp_quad2_kernel<40, true>);
+    touch_kernel(bp_quad2_kernel<72, true>);
 }
 
 void set_bp_variant(int walk, int raster)

@@ -142,8 +142,9 @@ def _check(st: int) -> None:
 
 
 def set_bp_variant(walk: int = 0, raster: int = 0) -> None:
-    """Speed-tuning hook (A/B runs, tests): pick a back-projection walk among the variants
-    that are bitwise equal to the automatic one, and the CTA raster band; 0 = automatic."""
+    """Speed-tuning hook (A/B runs, tests): pick a back-projection walk (include/ifdk.h lists
+    the families; variants within a family are bitwise equal) and the CTA raster band;
+    0 = automatic."""
     _check(_lib.ifdk_set_bp_variant(int(walk), int(raster)))
 
 
