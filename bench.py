@@ -168,8 +168,8 @@ def walk_smem_bytes(spec):
     """Algorithmic shared-memory bytes per update and kernel of the k-walk the library picks
     for the geometry: per 64-slice chunk and view a thread issues LDS.32
     taps -- QUAD (0.5 <= dv/dk < 1): eight 4+4-slice groups x 20 taps = 640 B / 64 updates =
-    10 B; 3-row TRIPLE (dv/dk < 0.5): ten 3+3-slice groups x 12 + a PAIR quad x 12 taps =
-    8.25 B; PAIR: 12 taps per 4 updates = 12 B."""
+    10 B; QUINT (dv/dk < 0.5): six 5+5-slice groups x 16 taps + a 2+2-slice tail x 12 taps =
+    432 B / 64 = 6.75 B; PAIR: 12 taps per 4 updates = 12 B."""
     import math
 
     r = math.hypot(spec.Nx * spec.Dx, spec.Ny * spec.Dy) / 2
@@ -177,7 +177,7 @@ def walk_smem_bytes(spec):
     if min(dv) >= 0.5001 and max(dv) < 0.9999:
         return 10.0, "QUAD", "bp_quad2_kernel"
     if max(dv) < 0.4999:
-        return 8.25, "3-row TRIPLE", "bp_tmem2_kernel"
+        return 6.75, "QUINT", "bp_quad2_kernel"
     return 12.0, "PAIR", "bp_raw_kernel"
 
 

@@ -116,14 +116,17 @@ struct __align__(16) Meta {
     double P[10];
     int u_org, v_org;    // box origin (detector column, row)
     int w_need, h_need;  // columns / rows of the box the tile x chunk can touch
-    int fast;            // the patch fits the box
-    // QUAD walk (WALK 13): the tile corner's invariants in fp64, split (u_c = uci + ucf,
-    // v_c(kb) = vci + vcf), the corner's u_c, v_c, z_c rounded to fp32 and the used entries of
-    // P_s rounded to fp32 -- each thread adds its small offset from the corner in fp32
+    // QUAD / QUINT walks (WALK 13): the tile corner's invariants in fp64, split (u_c = uci +
+    // ucf, v_c(kb) = vci + vcf), the corner's u_c, v_c, z_c rounded to fp32 and the used entries
+    // of P_s rounded to fp32 -- each thread adds its small offset from the corner in fp32.
+    // Laid out in 16-byte quads so a thread reads them with three 128-bit loads.
     int uci, vci;
-    float ucf, vcf, uc, vc, zc;
-    float p0, p1, p3, p4, p5, p7, p8;
-    int pad[3];
+    float ucf, vcf;
+    float uc, vc, zc, p0;
+    float p1, p3, p4, p5;
+    float p7, p8;
+    int fast;            // the patch fits the box
+    int pad;
 };
 
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -1737,9 +1740,124 @@ __device__ __forceinline__ void walk_views_quad2(uint32_t tacc, uint32_t a0, con
     quad_sub2<BW, 6>(tacc, a0, t, a1, u);
 }
 
+// QUINT walk (walk 14, the default where dv/dk < 1/2, config 5): runs of five slices around a
+// base floor n; slice b + j, j = -2..2, lies within one row of row n + r_j, r = (0, 0, 0, 1, 1),
+// exactly when dv < 1/2 (g_j = f_v + j dv - r_j in [-1, 1)).  Four rows n-1 .. n+2 feed five
+// slices: 1.6 LDS.32 per update (the 3-row TRIPLE: 2.0).  Halves at b = 10 q + 2 and 10 q + 7
+// (slices 10 q .. 10 q + 9), six groups and a two-slice-pair tail (60, 61 | 62, 63) from rows
+// n .. n+2.
+template <int BW, int Q0, int NQ>
+__device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, const ThreadInv& t)
+{
+    constexpr uint32_t S = BW * 4;
+    const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
+    const f2x du2 = pk2(t.du, t.du);
+    const f2x magic2 = pk2(8388608.0f, 8388608.0f), nmagic2 = pk2(-8388608.0f, -8388608.0f);
+    const f2x fv02 = pk2(t.fv0, t.fv0);
+    f2x kvec = pk2((float)(10 * Q0 + 2), (float)(10 * Q0 + 7));
+    asm volatile("mov.b64 %0, %0;" : "+l"(kvec));
+#pragma unroll
+    for (int qq = 0; qq < NQ; ++qq) {
+        const f2x v = fma2(kvec, dv2, fv02);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(kvec) : "l"(pk2(10.f, 10.f)));
+        const f2x tb = add2_rd(v, magic2);
+        const f2x fr = sub2(v, add2(tb, nmagic2));
+        const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+        const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+        f2x h[4];  // rows n-1 .. n+2
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const f2x a = pk2(lds32(adA + (r - 1) * S), lds32(adB + (r - 1) * S));
+            const f2x b = pk2(lds32(adA + (r - 1) * S + 4), lds32(adB + (r - 1) * S + 4));
+            h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
+        }
+        const f2x d0 = sub2(h[1], h[0]), d1 = sub2(h[2], h[1]), d2 = sub2(h[3], h[2]);
+        const f2x gm1 = sub2(fr, dv2);    // slice b - 1 from row n
+        const f2x gm2 = sub2(gm1, dv2);   // slice b - 2 from row n
+        const f2x g1 = add2(fr, dvm12);   // slice b + 1 from row n + 1
+        const f2x g2 = add2(g1, dv2);     // slice b + 2 from row n + 1
+        acc[5 * qq] = fma2(W2, fma2(gm2, sel2(d1, d0, gm2), h[1]), acc[5 * qq]);  // line 6;
+        acc[5 * qq + 1] = fma2(W2, fma2(gm1, sel2(d1, d0, gm1), h[1]), acc[5 * qq + 1]);
+        acc[5 * qq + 2] = fma2(W2, fma2(fr, d1, h[1]), acc[5 * qq + 2]);  // Alg. alg:bp line 10
+        acc[5 * qq + 3] = fma2(W2, fma2(g1, sel2(d2, d1, g1), h[2]), acc[5 * qq + 3]);
+        acc[5 * qq + 4] = fma2(W2, fma2(g2, sel2(d2, d1, g2), h[2]), acc[5 * qq + 4]);
+    }
+}
+
+// Slices 60, 61 (low half) and 62, 63 (high half) from rows n .. n+2 of their floors.
+template <int BW>
+__device__ __forceinline__ void quint_tail(f2x (&acc)[2], uint32_t a0, const ThreadInv& t)
+{
+    constexpr uint32_t S = BW * 4;
+    const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
+    const f2x du2 = pk2(t.du, t.du);
+    const f2x magic2 = pk2(8388608.0f, 8388608.0f), nmagic2 = pk2(-8388608.0f, -8388608.0f);
+    const f2x v = fma2(pk2(60.f, 62.f), dv2, pk2(t.fv0, t.fv0));
+    const f2x tb = add2_rd(v, magic2);
+    const f2x fr = sub2(v, add2(tb, nmagic2));
+    const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
+    const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
+    f2x h[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+        const f2x a = pk2(lds32(adA + r * S), lds32(adB + r * S));
+        const f2x b = pk2(lds32(adA + r * S + 4), lds32(adB + r * S + 4));
+        h[r] = fma2(du2, sub2(b, a), a);
+    }
+    const f2x d01 = sub2(h[1], h[0]), d12 = sub2(h[2], h[1]);
+    const f2x g = add2(fr, dvm12);
+    acc[0] = fma2(W2, fma2(fr, d01, h[0]), acc[0]);
+    acc[1] = fma2(W2, fma2(g, sel2(d12, d01, g), h[1]), acc[1]);
+}
+
+// Two QUINT groups (20 TMEM columns: pair 5 q + m = slices 10 q + m / 10 q + 5 + m) of two views.
+template <int BW, int Q0>
+__device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
+                                           uint32_t a1, const ThreadInv& u)
+{
+    f2x acc[10];
+    {
+        f2x x[8], y[2];
+        tm_ld16(tacc + 10 * Q0, x);
+        tm_ld4(tacc + 10 * Q0 + 16, y);
+        tm_wait_ld();
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[m] = x[m];
+        acc[8] = y[0];
+        acc[9] = y[1];
+    }
+    quint_groups<BW, Q0, 2>(acc, a0, t);
+    quint_groups<BW, Q0, 2>(acc, a1, u);
+    {
+        f2x x[8], y[2];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[m] = acc[m];
+        y[0] = acc[8];
+        y[1] = acc[9];
+        tm_st16(tacc + 10 * Q0, x);
+        tm_st4(tacc + 10 * Q0 + 16, y);
+    }
+}
+
+template <int BW>
+__device__ __forceinline__ void walk_views_quint2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
+                                                  uint32_t a1, const ThreadInv& u)
+{
+    tm_wait_st();
+    quint_sub2<BW, 0>(tacc, a0, t, a1, u);
+    quint_sub2<BW, 2>(tacc, a0, t, a1, u);
+    quint_sub2<BW, 4>(tacc, a0, t, a1, u);
+    f2x acc[2];
+    tm_ld4(tacc + 60, acc);
+    tm_wait_ld();
+    quint_tail<BW>(acc, a0, t);
+    quint_tail<BW>(acc, a1, u);
+    tm_st4(tacc + 60, acc);
+}
+
 // Flush of the QUAD accumulators: slices of the slab only (a partial chunk's other slices
 // were walked but are not written), zeros back.
-template <bool RED>
+template <bool RED, int RUN>
 __device__ __forceinline__ void flush_quad(uint32_t tacc, const BPParams& p, int i, int j, int kb,
                                            bool overwrite, bool inside)
 {
@@ -1759,7 +1877,9 @@ __device__ __forceinline__ void flush_quad(uint32_t tacc, const BPParams& p, int
                 const int pi = 8 * part + m;
 #pragma unroll
                 for (int half = 0; half < 2; ++half) {
-                    const int kk = 8 * (pi / 4) + 4 * half + pi % 4;
+                    const int kk = RUN == 4 ? 8 * (pi / 4) + 4 * half + pi % 4
+                                   : pi < 30 ? 10 * (pi / 5) + 5 * half + pi % 5
+                                             : 60 + 2 * half + (pi - 30);
                     const float v = half ? hi2(a[m]) : lo2(a[m]);
                     if (kk >= klo && kk < khi)
                         put_voxel<RED>(p, q0 + kk * plane, kb + kk, j, i, v, overwrite);
@@ -1772,7 +1892,7 @@ __device__ __forceinline__ void flush_quad(uint32_t tacc, const BPParams& p, int
 
 // The two-views-per-step TMEM kernel (bp_tmem2_kernel's pipeline) with the QUAD walk; whole and
 // partial chunks alike.
-template <int BW, bool RED = false>
+template <int BW, bool RED = false, int RUN = 4>
 __global__ void __launch_bounds__(kThreads, 3)
     bp_quad2_kernel(const __grid_constant__ BPParams p, const __grid_constant__ CUtensorMap tmap,
                     const __grid_constant__ PTable pt)
@@ -1856,12 +1976,15 @@ __global__ void __launch_bounds__(kThreads, 3)
                             (uint32_t)(((ti.nv - m0.v_org) * BW + (ti.nu - m0.u_org)) * 4) + nm;
         const uint32_t a1 = raw0 + (uint32_t)((te % NB) * p.raw_bytes) +
                             (uint32_t)(((tu.nv - m1.v_org) * BW + (tu.nu - m1.u_org)) * 4) + nm;
-        walk_views_quad2<BW>(tacc, a0, ti, a1, tu);
+        if constexpr (RUN == 4)
+            walk_views_quad2<BW>(tacc, a0, ti, a1, tu);
+        else
+            walk_views_quint2<BW>(tacc, a0, ti, a1, tu);
         if ((te >= first_flush && ((te - first_flush) & (VB - 1)) == 0) || te == n - 1) {
             const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
             const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
             const bool ow = !p.accumulate && te <= first_flush;
-            flush_quad<RED>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
+            flush_quad<RED, RUN>(tacc, p, fi, fj, kb, ow, fi < p.Nx && fj < p.Ny);
         }
         if (te + NB >= meta_next && meta_next < n) {
             metas(meta_next);
@@ -1953,11 +2076,12 @@ int choose_walk(const ifdk_geometry* g)
     if (!use_pair(g)) return 1;
     const double dv_min = g->D / g->Dv * g->Dz / g->zmax;
     const double dv_max = g->D / g->Dv * g->Dz / g->zmin;
-    int w = dv_min >= 0.5001 && dv_max < 0.9999 ? 13 : dv_max < 0.4999 ? 12 : 5;
+    int w = dv_min >= 0.5001 && dv_max < 0.9999 ? 13 : dv_max < 0.4999 ? 14 : 5;
     const int v = g_walk_override.load(std::memory_order_relaxed);
     if (v == 2 || v == 4 || v == 5) w = v;
     if ((v == 3 || v == 6 || v == 9 || v == 11) && dv_min >= 0.5001) w = v;
     if (v == 13 && dv_min >= 0.5001 && dv_max < 0.9999) w = v;
+    if (v == 14 && dv_max < 0.4999) w = v;
     if ((v == 7 || v == 8 || v == 10 || v == 12) && dv_max < 0.4999) w = v;
     return w;
 }
@@ -2030,7 +2154,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         int box_w = box_w0, P2 = 0, BW = 0;
         for (int c : {24, 40, 56, 72})
             if (c >= box_w - 1) { P2 = c; break; }
-        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 13)) {
+        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 14)) {
             for (int c : {40, 72})  // row pitch = 8 mod 32 words: conflict-free LDS.32 taps
                 if (c >= box_w) { BW = c; break; }
             box_w = BW;
@@ -2075,9 +2199,11 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         q.neg_magic = 0u - 0x4B000000u * (uint32_t)(BW ? BW * 4 : P2 * 8);
         dim3 grid((unsigned)(q.raster * tiles_j), (unsigned)nch,
                   (unsigned)((q.tiles_i + q.raster - 1) / q.raster));
-        if (BW && w == 13) {
-            auto k = q.red ? (BW == 40 ? bp_quad2_kernel<40, true> : bp_quad2_kernel<72, true>)
-                           : (BW == 40 ? bp_quad2_kernel<40> : bp_quad2_kernel<72>);
+        if (BW && (w == 13 || w == 14)) {
+            auto k = w == 13 ? (q.red ? (BW == 40 ? bp_quad2_kernel<40, true> : bp_quad2_kernel<72, true>)
+                                      : (BW == 40 ? bp_quad2_kernel<40> : bp_quad2_kernel<72>))
+                             : (q.red ? (BW == 40 ? bp_quad2_kernel<40, true, 5> : bp_quad2_kernel<72, true, 5>)
+                                      : (BW == 40 ? bp_quad2_kernel<40, false, 5> : bp_quad2_kernel<72, false, 5>));
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp quad)");
@@ -2164,16 +2290,16 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         }
     };
 
-    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 13)) || !tma_ok || box_w0 > 72)
+    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 14)) || !tma_ok || box_w0 > 72)
         return run(walk, p.kb0, n_chunks);
-    if (walk == 13) {
+    if (walk == 13 || walk == 14) {
         // the QUAD kernel walks partial chunks itself (one launch for the slab) when its six
         // boxes fit three CTAs per SM; otherwise the TRIPLE family (walk 11 + companions)
         const int bw = box_w0 <= 40 ? 40 : 72;
         const size_t raw_bytes = ((size_t)bw * box_h * 4 + 127) / 128 * 128;
         const size_t smem6 = kRawBuf2 * raw_bytes + kMetaRing * sizeof(Meta) + 8 * kRawBuf2 + 16;
-        if (3 * (smem6 + 1024) <= 228 * 1024) return run(13, p.kb0, n_chunks);
-        walk = 11;
+        if (3 * (smem6 + 1024) <= 228 * 1024) return run(walk, p.kb0, n_chunks);
+        walk = walk == 13 ? 11 : 12;
     }
     // RAW staging runs the whole chunks; a partial chunk at either slab end (its masked slices
     // would read rows outside the box) takes the x2 pair walk, bitwise the same values.
@@ -2245,6 +2371,10 @@ void preload_bp_kernels()
     touch_kernel(bp_quad2_kernel<72>);
     touch_kernel(bp_quad2_kernel<40, true>);
     touch_kernel(bp_quad2_kernel<72, true>);
+    touch_kernel(bp_quad2_kernel<40, false, 5>);
+    touch_kernel(bp_quad2_kernel<72, false, 5>);
+    touch_kernel(bp_quad2_kernel<40, true, 5>);
+    touch_kernel(bp_quad2_kernel<72, true, 5>);
 }
 
 void set_bp_variant(int walk, int raster)

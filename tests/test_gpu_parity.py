@@ -559,6 +559,7 @@ def test_bp_tmem_walks_view_ranges(torch_cuda, auto_variant, family, walks, dims
     ("3-row TRIPLE", ("12", "7", "8", "10"), (48, 96, 120, 48, 40, 256)),  # dv/dk 0.28-0.36
     ("PAIR", ("5", "4", "2"), (48, 96, 192, 48, 40, 256)),      # dv/dk in [0.45, 0.58]
     ("QUAD", ("13",), (48, 96, 256, 48, 40, 256)),              # masked partial chunks
+    ("QUINT", ("14",), (48, 96, 120, 48, 40, 256)),             # masked partial chunks
 ])
 def test_bp_partial_chunks_far_into_the_chunk(torch_cuda, auto_variant, family, walks, dims):
     """Slab cuts deep inside a 64-slice chunk (k0 % 64 in {57, 59, 63}, ends 1, 3, 5 slices
@@ -593,16 +594,20 @@ def test_bp_partial_chunks_far_into_the_chunk(torch_cuda, auto_variant, family, 
     assert_parity(whole.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, f"bp {family} partial chunks")
 
 
-def test_bp_quad_walk(torch_cuda, auto_variant):
-    """QUAD walk (13, the default where 0.5 <= dv/dk < 1): it is the automatic choice for the
-    config-4 geometry; view ranges off the 128-view grid, odd lengths, one and two views and
-    ranges crossing the 256-view launch boundary match the oracle; calls cut at multiples of
-    the 128-view summation batch are bitwise one call; slab splits (the kernel walks partial
-    chunks itself, masked write-back) are bitwise the whole volume."""
+@pytest.mark.parametrize("walk,dims", [
+    (13, (600, 96, 256, 48, 40, 128)),  # QUAD: dv/dk in [0.60, 0.77] (configs 1-4)
+    (14, (600, 96, 120, 48, 40, 128)),  # QUINT: dv/dk in [0.28, 0.36] (config 5)
+])
+def test_bp_quad_walk(torch_cuda, auto_variant, walk, dims):
+    """QUAD / QUINT walks (13 / 14, the defaults where 0.5 <= dv/dk < 1 / dv/dk < 0.5): the
+    automatic choice for their geometry; view ranges off the 128-view grid, odd lengths, one
+    and two views and ranges crossing the 256-view launch boundary match the oracle; calls cut
+    at multiples of the 128-view summation batch are bitwise one call; slab splits (the kernel
+    walks partial chunks itself, masked write-back) are bitwise the whole volume."""
     torch = torch_cuda
     from paper_1909_02724_b200 import Geometry, ifdk_backproject, set_bp_variant
 
-    spec = _spec(600, 96, 256, 48, 40, 128)  # dv/dk in [0.60, 0.77]
+    spec = _spec(*dims)
     g = Geometry.from_spec(spec)
     Qn = _oracle_Q32(spec, _phantom_E(spec))
     Q = torch.from_numpy(Qn).cuda()
@@ -616,16 +621,16 @@ def test_bp_quad_walk(torch_cuda, auto_variant):
         return vol
 
     default = run(0, 0, 600)
-    assert torch.equal(default, run(13, 0, 600))
+    assert torch.equal(default, run(walk, 0, 600))
     for s0, n in ((0, 600), (1, 300), (37, 219), (127, 2), (128, 1), (1, 1), (0, 2), (5, 131)):
         ref = oracle.backproject_volume(og, Qn[s0:s0 + n].astype(np.float64), s0=s0, v0=0, k0=0,
                                         nk=spec.Nz)
-        assert_parity(run(13, s0, n).cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL,
-                      f"bp QUAD walk views {s0}..{s0 + n}")
+        assert_parity(run(walk, s0, n).cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL,
+                      f"bp walk {walk} views {s0}..{s0 + n}")
     for cuts in ((0, 128, 384, 600), (0, 256, 600)):
         part = torch.empty_like(default)
         for a, b in zip(cuts[:-1], cuts[1:]):
-            run(13, a, b - a, out=part, acc=a > 0)
+            run(walk, a, b - a, out=part, acc=a > 0)
         assert torch.equal(part, default), cuts
     for a, b in ((0, 77), (77, 128), (3, 125), (64, 65), (57, 70)):
-        assert torch.equal(run(13, 0, 600, k0=a, nk=b - a), default[a:b]), (a, b)
+        assert torch.equal(run(walk, 0, 600, k0=a, nk=b - a), default[a:b]), (a, b)

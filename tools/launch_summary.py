@@ -8,7 +8,7 @@ import collections
 import csv
 import sys
 
-FDK = ("bp_tmem2_kernel", "bp_tmem_kernel", "bp_raw_kernel", "bp_kernel", "filter_f4k_kernel",
+FDK = ("bp_quad2_kernel", "bp_tmem2_kernel", "bp_tmem_kernel", "bp_raw_kernel", "bp_kernel", "filter_f4k_kernel",
        "filter_fft_kernel")
 
 
