@@ -296,8 +296,10 @@ ifdk_status ifdk_fill(float* x_dev, float value, long n, void* stream);
  * keep the accumulators in tensor memory, 11 / 12 step two views at a time), and
  * the QUAD walk 13 (the automatic choice where 0.5 <= dv/dk < 1: four slices per
  * floor, tensor-memory accumulators, two views per step, partial chunks in the
- * same kernel) is its own family -- it agrees with the others to fp32 rounding,
- * not bitwise.  A walk outside the geometry's range, or 0,
+ * same kernel), the QUINT walk 14 (five slices per floor, the automatic choice
+ * where dv/dk < 0.5) and QUINT-HI 15 (five slices where 0.5 <= dv/dk < 1) are
+ * families of their own -- they agree with the others to fp32 rounding, not
+ * bitwise.  A walk outside the geometry's range, or 0,
  * means automatic.
  * raster sets the CTA raster band in tiles (0 = automatic; >= the tile count =
  * row-major); it only reorders CTAs.  Process-wide; affects later launches. */

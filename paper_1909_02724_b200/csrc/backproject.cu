@@ -581,7 +581,7 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
         vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
-    if (WALK == 13 && lane == 0) {  // lane 0 holds the tile corner (i_corner, j_corner) = base
+    if (WALK >= 13 && lane == 0) {  // lane 0 holds the tile corner (i_corner, j_corner) = base
         const double fu = floor(c.u), fv = floor(c.v);
         m->uci = (int)fu;
         m->vci = (int)fv;
@@ -600,8 +600,9 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
         // rounded down to a multiple of 4 floats.
         const bool finite = fu0 > -1e9 && fu1 < 1e9 && fv0 > -1e9 && fv1 < 1e9;
         const int u_org = finite ? (((int)fu0 - 1) & ~3) : 0;
-        // QUAD: one more row below (its fp32 thread floors may sit one below the corners')
-        constexpr int MV = WALK == 13 ? 1 : 0;
+        // QUAD / QUINT: one more row below (their fp32 thread floors may sit one below the
+        // corners'), two for the HI runs that reach row n-2
+        constexpr int MV = WALK == 13 ? 1 : WALK == 15 ? 2 : 0;
         const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0 + p.pair + MV;
         const bool fits = finite && w_need <= p.box_w && h_need <= p.box_h;
         m->u_org = u_org;
@@ -1746,7 +1747,10 @@ __device__ __forceinline__ void walk_views_quad2(uint32_t tacc, uint32_t a0, con
 // slices: 1.6 LDS.32 per update (the 3-row TRIPLE: 2.0).  Halves at b = 10 q + 2 and 10 q + 7
 // (slices 10 q .. 10 q + 9), six groups and a two-slice-pair tail (60, 61 | 62, 63) from rows
 // n .. n+2.
-template <int BW, int Q0, int NQ>
+// HI (walk 15, 0.5 <= dv/dk < 1): the same five-slice runs reach rows n-2 .. n+3, r = (-1, 0,
+// 0, 1, 2) -- g_j in [-1, 1) exactly when 0.5 <= dv <= 1: six rows per five slices, 2.4 LDS.32
+// per update (QUAD 2.5) but a 2+2 tail per chunk.
+template <int BW, int Q0, int NQ, bool HI = false>
 __device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, const ThreadInv& t)
 {
     constexpr uint32_t S = BW * 4;
@@ -1764,23 +1768,35 @@ __device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, co
         const f2x fr = sub2(v, add2(tb, nmagic2));
         const uint32_t adA = __float_as_uint(lo2(tb)) * S + a0;
         const uint32_t adB = __float_as_uint(hi2(tb)) * S + a0;
-        f2x h[4];  // rows n-1 .. n+2
+        constexpr int NR = HI ? 6 : 4, R0 = HI ? 2 : 1;  // rows n-R0 .. n-R0+NR-1
+        f2x h[NR];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            const f2x a = pk2(lds32(adA + (r - 1) * S), lds32(adB + (r - 1) * S));
-            const f2x b = pk2(lds32(adA + (r - 1) * S + 4), lds32(adB + (r - 1) * S + 4));
+        for (int r = 0; r < NR; ++r) {
+            const f2x a = pk2(lds32(adA + (r - R0) * S), lds32(adB + (r - R0) * S));
+            const f2x b = pk2(lds32(adA + (r - R0) * S + 4), lds32(adB + (r - R0) * S + 4));
             h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
         }
-        const f2x d0 = sub2(h[1], h[0]), d1 = sub2(h[2], h[1]), d2 = sub2(h[3], h[2]);
+        f2x d[NR - 1];  // d[r] = h[r+1] - h[r]
+#pragma unroll
+        for (int r = 0; r < NR - 1; ++r) d[r] = sub2(h[r + 1], h[r]);
+        constexpr int N0 = R0;  // index of row n in h
         const f2x gm1 = sub2(fr, dv2);    // slice b - 1 from row n
-        const f2x gm2 = sub2(gm1, dv2);   // slice b - 2 from row n
         const f2x g1 = add2(fr, dvm12);   // slice b + 1 from row n + 1
-        const f2x g2 = add2(g1, dv2);     // slice b + 2 from row n + 1
-        acc[5 * qq] = fma2(W2, fma2(gm2, sel2(d1, d0, gm2), h[1]), acc[5 * qq]);  // line 6;
-        acc[5 * qq + 1] = fma2(W2, fma2(gm1, sel2(d1, d0, gm1), h[1]), acc[5 * qq + 1]);
-        acc[5 * qq + 2] = fma2(W2, fma2(fr, d1, h[1]), acc[5 * qq + 2]);  // Alg. alg:bp line 10
-        acc[5 * qq + 3] = fma2(W2, fma2(g1, sel2(d2, d1, g1), h[2]), acc[5 * qq + 3]);
-        acc[5 * qq + 4] = fma2(W2, fma2(g2, sel2(d2, d1, g2), h[2]), acc[5 * qq + 4]);
+        if constexpr (HI) {
+            const f2x gm2 = sub2(gm1, dvm12);  // slice b - 2 from row n - 1
+            const f2x g2 = add2(g1, dvm12);    // slice b + 2 from row n + 2
+            acc[5 * qq] = fma2(W2, fma2(gm2, sel2(d[N0 - 1], d[N0 - 2], gm2), h[N0 - 1]), acc[5 * qq]);
+            acc[5 * qq + 4] = fma2(W2, fma2(g2, sel2(d[N0 + 2], d[N0 + 1], g2), h[N0 + 2]), acc[5 * qq + 4]);
+        } else {
+            const f2x gm2 = sub2(gm1, dv2);    // slice b - 2 from row n
+            const f2x g2 = add2(g1, dv2);      // slice b + 2 from row n + 1
+            acc[5 * qq] = fma2(W2, fma2(gm2, sel2(d[N0], d[N0 - 1], gm2), h[N0]), acc[5 * qq]);
+            acc[5 * qq + 4] = fma2(W2, fma2(g2, sel2(d[N0 + 1], d[N0], g2), h[N0 + 1]), acc[5 * qq + 4]);
+        }
+        // line 6 (the row lerp), Alg. alg:bp line 10 (the accumulation)
+        acc[5 * qq + 1] = fma2(W2, fma2(gm1, sel2(d[N0], d[N0 - 1], gm1), h[N0]), acc[5 * qq + 1]);
+        acc[5 * qq + 2] = fma2(W2, fma2(fr, d[N0], h[N0]), acc[5 * qq + 2]);
+        acc[5 * qq + 3] = fma2(W2, fma2(g1, sel2(d[N0 + 1], d[N0], g1), h[N0 + 1]), acc[5 * qq + 3]);
     }
 }
 
@@ -1811,7 +1827,7 @@ __device__ __forceinline__ void quint_tail(f2x (&acc)[2], uint32_t a0, const Thr
 }
 
 // Two QUINT groups (20 TMEM columns: pair 5 q + m = slices 10 q + m / 10 q + 5 + m) of two views.
-template <int BW, int Q0>
+template <int BW, int Q0, bool HI>
 __device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
                                            uint32_t a1, const ThreadInv& u)
 {
@@ -1826,8 +1842,8 @@ __device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const Thr
         acc[8] = y[0];
         acc[9] = y[1];
     }
-    quint_groups<BW, Q0, 2>(acc, a0, t);
-    quint_groups<BW, Q0, 2>(acc, a1, u);
+    quint_groups<BW, Q0, 2, HI>(acc, a0, t);
+    quint_groups<BW, Q0, 2, HI>(acc, a1, u);
     {
         f2x x[8], y[2];
 #pragma unroll
@@ -1839,14 +1855,14 @@ __device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const Thr
     }
 }
 
-template <int BW>
+template <int BW, bool HI>
 __device__ __forceinline__ void walk_views_quint2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
                                                   uint32_t a1, const ThreadInv& u)
 {
     tm_wait_st();
-    quint_sub2<BW, 0>(tacc, a0, t, a1, u);
-    quint_sub2<BW, 2>(tacc, a0, t, a1, u);
-    quint_sub2<BW, 4>(tacc, a0, t, a1, u);
+    quint_sub2<BW, 0, HI>(tacc, a0, t, a1, u);
+    quint_sub2<BW, 2, HI>(tacc, a0, t, a1, u);
+    quint_sub2<BW, 4, HI>(tacc, a0, t, a1, u);
     f2x acc[2];
     tm_ld4(tacc + 60, acc);
     tm_wait_ld();
@@ -1931,7 +1947,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     };
     auto metas = [=](int t0) {  // boxes of the whole chunk (partial chunks too)
         if (t0 + warp < n)
-            compute_meta1<KC, 13>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner,
+            compute_meta1<KC, RUN == 6 ? 15 : 13>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner,
                                   kb, 0, KC);
     };
 
@@ -1979,7 +1995,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         if constexpr (RUN == 4)
             walk_views_quad2<BW>(tacc, a0, ti, a1, tu);
         else
-            walk_views_quint2<BW>(tacc, a0, ti, a1, tu);
+            walk_views_quint2<BW, RUN == 6>(tacc, a0, ti, a1, tu);
         if ((te >= first_flush && ((te - first_flush) & (VB - 1)) == 0) || te == n - 1) {
             const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
             const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
@@ -2082,6 +2098,7 @@ int choose_walk(const ifdk_geometry* g)
     if ((v == 3 || v == 6 || v == 9 || v == 11) && dv_min >= 0.5001) w = v;
     if (v == 13 && dv_min >= 0.5001 && dv_max < 0.9999) w = v;
     if (v == 14 && dv_max < 0.4999) w = v;
+    if (v == 15 && dv_min >= 0.5001 && dv_max < 0.9999) w = v;
     if ((v == 7 || v == 8 || v == 10 || v == 12) && dv_max < 0.4999) w = v;
     return w;
 }
@@ -2134,7 +2151,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
     patch_bound(g, kTI, kTJ, KC, &wb, &hb);
     p.pair = use_pair(g) ? 1 : 0;
     int walk = KC == 64 ? choose_walk(g) : (p.pair ? 2 : 1);
-    const int box_h = (int)std::ceil(hb) + 6 + p.pair;
+    const int box_h = (int)std::ceil(hb) + 6 + p.pair + (walk == 15 ? 1 : 0);
     const int box_w0 = std::max(8, ((int)std::ceil(wb) + 9 + 3) / 4 * 4);  // +3: 16-B origin
     // Raster band of 16 tile columns: measured on B200 (config 4, one 256-view launch) DRAM
     // traffic 49 GB (algorithmic 39 GB) and L2 hit rate 95 %, vs 354 GB and 65 % for the
@@ -2154,7 +2171,7 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         int box_w = box_w0, P2 = 0, BW = 0;
         for (int c : {24, 40, 56, 72})
             if (c >= box_w - 1) { P2 = c; break; }
-        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 14)) {
+        if (w == 5 || w == 6 || w == 7 || (w >= 9 && w <= 15)) {
             for (int c : {40, 72})  // row pitch = 8 mod 32 words: conflict-free LDS.32 taps
                 if (c >= box_w) { BW = c; break; }
             box_w = BW;
@@ -2199,11 +2216,13 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         q.neg_magic = 0u - 0x4B000000u * (uint32_t)(BW ? BW * 4 : P2 * 8);
         dim3 grid((unsigned)(q.raster * tiles_j), (unsigned)nch,
                   (unsigned)((q.tiles_i + q.raster - 1) / q.raster));
-        if (BW && (w == 13 || w == 14)) {
+        if (BW && (w == 13 || w == 14 || w == 15)) {
             auto k = w == 13 ? (q.red ? (BW == 40 ? bp_quad2_kernel<40, true> : bp_quad2_kernel<72, true>)
                                       : (BW == 40 ? bp_quad2_kernel<40> : bp_quad2_kernel<72>))
-                             : (q.red ? (BW == 40 ? bp_quad2_kernel<40, true, 5> : bp_quad2_kernel<72, true, 5>)
-                                      : (BW == 40 ? bp_quad2_kernel<40, false, 5> : bp_quad2_kernel<72, false, 5>));
+                   : w == 14 ? (q.red ? (BW == 40 ? bp_quad2_kernel<40, true, 5> : bp_quad2_kernel<72, true, 5>)
+                                      : (BW == 40 ? bp_quad2_kernel<40, false, 5> : bp_quad2_kernel<72, false, 5>))
+                             : (q.red ? (BW == 40 ? bp_quad2_kernel<40, true, 6> : bp_quad2_kernel<72, true, 6>)
+                                      : (BW == 40 ? bp_quad2_kernel<40, false, 6> : bp_quad2_kernel<72, false, 6>));
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(bp quad)");
@@ -2290,16 +2309,16 @@ ifdk_status launch_range(const ifdk_geometry* g, const float* Q, long s0, long n
         }
     };
 
-    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 14)) || !tma_ok || box_w0 > 72)
+    if ((walk != 5 && walk != 6 && walk != 7 && (walk < 9 || walk > 15)) || !tma_ok || box_w0 > 72)
         return run(walk, p.kb0, n_chunks);
-    if (walk == 13 || walk == 14) {
+    if (walk >= 13 && walk <= 15) {
         // the QUAD kernel walks partial chunks itself (one launch for the slab) when its six
         // boxes fit three CTAs per SM; otherwise the TRIPLE family (walk 11 + companions)
         const int bw = box_w0 <= 40 ? 40 : 72;
         const size_t raw_bytes = ((size_t)bw * box_h * 4 + 127) / 128 * 128;
         const size_t smem6 = kRawBuf2 * raw_bytes + kMetaRing * sizeof(Meta) + 8 * kRawBuf2 + 16;
         if (3 * (smem6 + 1024) <= 228 * 1024) return run(walk, p.kb0, n_chunks);
-        walk = walk == 13 ? 11 : 12;
+        walk = walk == 14 ? 12 : 11;
     }
     // RAW staging runs the whole chunks; a partial chunk at either slab end (its masked slices
     // would read rows outside the box) takes the x2 pair walk, bitwise the same values.
@@ -2375,6 +2394,10 @@ void preload_bp_kernels()
     touch_kernel(bp_quad2_kernel<72, false, 5>);
     touch_kernel(bp_quad2_kernel<40, true, 5>);
     touch_kernel(bp_quad2_kernel<72, true, 5>);
+    touch_kernel(bp_quad2_kernel<40, false, 6>);
+    touch_kernel(bp_quad2_kernel<72, false, 6>);
+    touch_kernel(bp_quad2_kernel<40, true, 6>);
+    touch_kernel(bp_quad2_kernel<72, true, 6>);
 }
 
 void set_bp_variant(int walk, int raster)
