@@ -5,31 +5,33 @@
 //
 // Mapping (B200-first; not the paper's shflBP design):
 //  * A CTA (256 threads = 8 warps of 8(i) x 4(j) columns) owns a 16 x 16 column tile and a
-//    KC-slice k-chunk aligned to global multiples of KC.  Each thread owns one voxel column
-//    and walks the chunk with KC register accumulators: per (column, view) it computes
-//    z, u, 1/z^2 and the base of v in fp64 once, then per update
-//    only v = fv0 + kappa dv in fp32, a floor, two shared-memory loads and four FMAs.
+//    64-slice k-chunk aligned to global multiples of 64.  Each thread owns one voxel column;
+//    per (column, view) it forms u, the base of v, dv/dk and 1/z^2 once, then per update only
+//    v = fv0 + kappa dv in fp32, a floor, shared-memory tap loads and packed fp32x2 FMAs.
 //  * The detector patch the tile x chunk projects onto (its extent is bounded from the
 //    tile corners: u, v are linear-fractional, so extremes sit at corners) is staged per
 //    view by TMA (cp.async.bulk.tensor, OOB zero fill = the per-tap zero border, reading
-//    c-A9).  Default (bp_raw_kernel, walk 5): four boxes in flight per CTA and the walk
-//    reads both taps of a row straight from the box (two LDS.32, row pitch 8 mod 32 words);
-//    the PAIR walk (two slices per floor) runs on packed fp32x2 instructions.  Variants
-//    (bp_kernel, walks 1-4): a double-buffered box rewritten once into (Q[r][c], Q[r][c+1] -
-//    Q[r][c]) pairs (one LDS.64 per row), scalar or fp32x2 walks; walk 4 also serves the
-//    partial chunks at slab ends for walk 5.  All PAIR variants are bitwise equal.
+//    c-A9) into a ring of boxes (mbarrier completion); the walk reads both taps of a row
+//    straight from the box (two LDS.32, row pitch 8 mod 32 words: conflict-free).
+//  * Default (bp_quad2_kernel, walks 13 / 14): runs of four (QUAD, 0.5 <= dv/dk < 1) or five
+//    (QUINT, dv/dk < 1/2) slices share one floor; the 64 partial sums of a thread live in
+//    tensor memory (tcgen05.alloc / ld / st), two views per step, three CTAs per SM; the
+//    per-(column, view) invariants are fp32 offsets from the tile corner's fp64 values; slab
+//    ends inside a chunk are walked by the same kernel with a masked write-back.  Variants
+//    (A/B and tests, ifdk_set_bp_variant): the TRIPLE family (bp_tmem2_kernel, bp_tmem_kernel,
+//    bp_raw_kernel, pair-patch companions in bp_kernel for partial chunks; fp64 per-thread
+//    invariants, bitwise equal to each other) and the PAIR family (walks 2, 4, 5).
 //  * P_s lives in constant memory: each launch carries the fp64 rows of its <= 256 views in
 //    a __grid_constant__ kernel parameter (param space = the constant bank), so no
 //    per-launch device allocation or host-to-device copy is needed.  Longer view ranges are
 //    split into launches at global multiples of 256 views, which are also flush points of
 //    the two-level summation, so the split does not change a bit.
-//  * Views are summed in order; every VB views (aligned to global view index) the register
+//  * Views are summed in order; every VB = 128 views (aligned to the global view index) the
 //    partial sums are added to the volume, a two-level summation.
 //  * The box is sized from a conservative geometric bound (patch_bound), so every view's
 //    patch fits it; a violation is a bug and traps (it kills the CUDA context).  Geometries
 //    whose box cannot be described to TMA or exceeds the opt-in shared memory (N_u % 4 != 0,
-//    box taller than 256 rows or too large) take the same walk with taps read from global
-//    memory, bitwise-identical arithmetic.
+//    box taller than 256 rows or too large) take a walk with taps read from global memory.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
