@@ -641,16 +641,19 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
         __syncthreads();  // exchange written, staging read out: fetch the next group meanwhile
         prefetch(gi + gridDim.x);
         fwd_s3(u, A, tmw, i);
-        // Y = X . H (real, even; C/L folded in), conj for the inverse-by-forward trick.
+        // Y = X . H (real, even; C/L folded in), and the inverse by the forward transform:
+        // DFT(i conj(Y)) = i conj(L z) = (im L z, re L z) -- multiplying conj(Y) by i swaps the
+        // halves (free, a .LO_HI operand), and the transform then returns row B's samples in
+        // the real halves and row A's in the imaginary ones, with no negation left anywhere.
 #pragma unroll
         for (int d = 0; d < 16; ++d) {
             const float h = Hp[256 * d + i];
-            u[d] = cmul2(u[d], mk(h, -h));
+            u[d] = cmul2(mk(im_(u[d]), re_(u[d])), mk(h, h));
         }
         inv_s3(u, A, tmw, i);
         __syncthreads();
         inv_s1(u, A, tmw, i);
-        // Q = conj(Z): real -> row A, -imag -> row B of each slot, samples 0..Nu-1 (to every
+        // Q: imaginary halves -> row A, real halves -> row B of each slot, samples 0..Nu-1 (to every
         // destination band that holds the row when scattering).
         if (p.n_dest == 0 && p.Nu == SLOT_F && r0 + ROWS <= p.n_rows_total) {
             // whole group of full-width rows (configs 2-4): row stride SLOT_F, no masks
@@ -659,8 +662,8 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
             for (int sl = 0; sl < R; ++sl)
 #pragma unroll
                 for (int jj = 0; jj < SJ / 2; ++jj) {
-                    q0[(2 * sl) * SLOT_F + jj * T] = re_(u[sl * SJ + jj]);
-                    q0[(2 * sl + 1) * SLOT_F + jj * T] = -im_(u[sl * SJ + jj]);
+                    q0[(2 * sl) * SLOT_F + jj * T] = im_(u[sl * SJ + jj]);
+                    q0[(2 * sl + 1) * SLOT_F + jj * T] = re_(u[sl * SJ + jj]);
                 }
         } else if (p.n_dest == 0) {
 #pragma unroll
@@ -674,8 +677,8 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
                 for (int jj = 0; jj < SJ / 2; ++jj) {
                     const int n = i + jj * T;
                     if (n < p.Nu) {
-                        qA[n] = re_(u[sl * SJ + jj]);
-                        if (hasB) qB[n] = -im_(u[sl * SJ + jj]);
+                        qA[n] = im_(u[sl * SJ + jj]);
+                        if (hasB) qB[n] = re_(u[sl * SJ + jj]);
                     }
                 }
             }
@@ -695,8 +698,8 @@ __global__ void __launch_bounds__(256, 3) filter_f4k_kernel(const FilterParams p
                     for (int jj = 0; jj < SJ / 2; ++jj) {
                         const int n = i + jj * T;
                         if (n < p.Nu) {
-                            if (qA) qA[n] = re_(u[sl * SJ + jj]);
-                            if (qB) qB[n] = -im_(u[sl * SJ + jj]);
+                            if (qA) qA[n] = im_(u[sl * SJ + jj]);
+                            if (qB) qB[n] = re_(u[sl * SJ + jj]);
                         }
                     }
                 }
