@@ -115,7 +115,7 @@ __device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, in
 }
 
 struct __align__(16) Meta {
-    double P[10];
+    double P[10];        // P_s (bp_kernel reads it from here, 128-bit loads)
     int u_org, v_org;    // box origin (detector column, row)
     int w_need, h_need;  // columns / rows of the box the tile x chunk can touch
     // QUAD / QUINT walks (WALK 13): the tile corner's invariants in fp64, split (u_c = uci +
@@ -583,18 +583,6 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
         vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
         vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
     }
-    if (WALK >= 13 && lane == 0) {  // lane 0 holds the tile corner (i_corner, j_corner) = base
-        const double fu = floor(c.u), fv = floor(c.v);
-        m->uci = (int)fu;
-        m->vci = (int)fv;
-        m->ucf = (float)(c.u - fu);
-        m->vcf = (float)(c.v - fv);
-        m->uc = (float)c.u;
-        m->vc = (float)c.v;
-        m->zc = (float)(1.0 / c.f);
-        m->p0 = (float)P[0]; m->p1 = (float)P[1]; m->p3 = (float)P[3]; m->p4 = (float)P[4];
-        m->p5 = (float)P[5]; m->p7 = (float)P[7]; m->p8 = (float)P[8];
-    }
     if (lane == 0) {
         const double fu0 = floor(umin), fu1 = floor(umax), fv0 = floor(vmin), fv1 = floor(vmax);
         // TMA (tile mode, no swizzle) faults unless the innermost box coordinate is a
@@ -602,9 +590,59 @@ __device__ void compute_meta1(Meta* ring, const BPParams& p, const double* Pc, i
         // rounded down to a multiple of 4 floats.
         const bool finite = fu0 > -1e9 && fu1 < 1e9 && fv0 > -1e9 && fv1 < 1e9;
         const int u_org = finite ? (((int)fu0 - 1) & ~3) : 0;
-        // QUAD / QUINT: one more row below (their fp32 thread floors may sit one below the
-        // corners'), two for the HI runs that reach row n-2
-        constexpr int MV = WALK == 13 ? 1 : WALK == 15 ? 2 : 0;
+        const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0 + p.pair;
+        const bool fits = finite && w_need <= p.box_w && h_need <= p.box_h;
+        m->u_org = u_org;
+        m->v_org = finite ? (int)fv0 - 1 : 0;
+        m->fast = fits ? 1 : 0;
+        m->w_need = fits ? (int)w_need : 0;
+        m->h_need = fits ? (int)h_need : 0;
+    }
+}
+
+// The metas of eight views in one warp (QUAD / QUINT kernel): lanes 4 v .. 4 v + 3 take view
+// t0 + v at the tile's four corner columns (the same arithmetic as compute_meta1 over the whole
+// chunk), so one warp does in one pass what eight warps did one view each.
+template <int KC, int WALK>
+__device__ void compute_meta8(Meta* ring, const BPParams& p, const PTable* pt, int t0, int n,
+                              int tile_i, int tile_j, int kb)
+{
+    const int lane = threadIdx.x & 31;
+    const int t = t0 + (lane >> 2);
+    const bool valid = t < n;
+    const double* Pc = pt->P[valid ? t : t0];
+    double P[10];
+#pragma unroll
+    for (int q = 0; q < 10; ++q) P[q] = Pc[q];
+    const int i_corner = (lane & 1) ? min(tile_i * 16 + 16, p.Nx) - 1 : tile_i * 16;
+    const int j_corner = (lane & 2) ? min(tile_j * 16 + 16, p.Ny) - 1 : tile_j * 16;
+    const ColInv c = column_invariants(P, (double)i_corner, (double)j_corner, (double)kb);
+    double umin = c.u, umax = c.u;
+    const double va = c.v, vb = c.v + (KC - 1) * c.dv;
+    double vmin = fmin(va, vb), vmax = fmax(va, vb);
+#pragma unroll
+    for (int o = 1; o < 4; o <<= 1) {  // within the view's four lanes
+        umin = fmin(umin, __shfl_xor_sync(0xffffffffu, umin, o));
+        umax = fmax(umax, __shfl_xor_sync(0xffffffffu, umax, o));
+        vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+    }
+    if (valid && (lane & 3) == 0) {  // the tile's base corner (i_corner, j_corner)
+        Meta* m = &ring[t & (kMetaRing - 1)];
+        const double fu = floor(c.u), fv = floor(c.v);
+        m->uci = (int)fu;
+        m->vci = (int)fv;
+        m->ucf = (float)(c.u - fu);
+        m->vcf = (float)(c.v - fv);
+        m->uc = (float)c.u;
+        m->vc = (float)c.v;
+        m->zc = (float)c.z;
+        m->p0 = (float)P[0]; m->p1 = (float)P[1]; m->p3 = (float)P[3]; m->p4 = (float)P[4];
+        m->p5 = (float)P[5]; m->p7 = (float)P[7]; m->p8 = (float)P[8];
+        const double fu0 = floor(umin), fu1 = floor(umax), fv0 = floor(vmin), fv1 = floor(vmax);
+        const bool finite = fu0 > -1e9 && fu1 < 1e9 && fv0 > -1e9 && fv1 < 1e9;
+        const int u_org = finite ? (((int)fu0 - 1) & ~3) : 0;  // 16-byte TMA origin
+        constexpr int MV = WALK == 15 ? 2 : 1;  // rows below: fp32 thread floors, HI runs
         const double w_need = fu1 + 3.0 - u_org, h_need = fv1 - fv0 + 4.0 + p.pair + MV;
         const bool fits = finite && w_need <= p.box_w && h_need <= p.box_h;
         m->u_org = u_org;
@@ -1947,10 +1985,9 @@ __global__ void __launch_bounds__(kThreads, 3)
         mbar_expect_tx(&mbar[b], tx_bytes);
         tma_load_3d(raw + b * p.raw_bytes, tmap_ptr, &mbar[b], m.u_org, m.v_org - p.v0, t);
     };
-    auto metas = [=](int t0) {  // boxes of the whole chunk (partial chunks too)
-        if (t0 + warp < n)
-            compute_meta1<KC, RUN == 6 ? 15 : 13>(meta, p, ptab->P[t0 + warp], t0 + warp, i_corner, j_corner,
-                                  kb, 0, KC);
+    auto metas = [=](int t0) {  // boxes of the whole chunk (partial chunks too), 8 views
+        if (warp == ((t0 >> 3) & 7))
+            compute_meta8<KC, RUN == 6 ? 15 : 13>(meta, p, ptab, t0, n, tile_i, tile_j, kb);
     };
 
     if (warp == 0) {

@@ -37,7 +37,7 @@ inline void fill_ptable(const ifdk_geometry* g, long s0, long n_views, PTable& p
 // chunk base kb; dv = dv/dk.  Shared by the threads and by the patch-bound computation so
 // that corner columns reproduce the threads' values bit for bit.
 struct ColInv {
-    double u, v, f, dv;
+    double u, v, f, dv, z;
 };
 
 __device__ __forceinline__ ColInv column_invariants(const double* P, double i, double j, double kb)
@@ -46,6 +46,7 @@ __device__ __forceinline__ ColInv column_invariants(const double* P, double i, d
     const double x = fma(P[0], i, fma(P[1], j, P[2]));
     const double y = fma(P[3], i, fma(P[4], j, fma(P[5], kb, P[6])));
     const double z = fma(P[7], i, fma(P[8], j, P[9]));
+    c.z = z;
     c.f = __drcp_rn(z);
     c.u = x * c.f;
     c.v = y * c.f;
