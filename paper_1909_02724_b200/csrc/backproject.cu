@@ -2017,20 +2017,35 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int first_flush = (int)(VB - 1 - (p.s0 % VB + VB) % VB);
     const float fdi = (float)(ic - tile_i * kTI), fdj = (float)(jc - tile_j * kTJ);
     const uint32_t nm = p.neg_magic;
+    // box ring position of view t (buffer, mbarrier phase), stepped without divisions
+    int bt = 0;
+    uint32_t pt0 = 0;
     for (int t = 0; t < n;) {
         const bool two = t + 1 < n && !(t == 0 && (first_flush & 1) == 0);
         const int te = two ? t + 1 : t;
+        int be = bt;
+        uint32_t pe = pt0;
+        if (two && ++be == NB) {
+            be = 0;
+            pe ^= 1u;
+        }
         const Meta& m0 = meta[t & (kMetaRing - 1)];
         const Meta& m1 = meta[te & (kMetaRing - 1)];
         const ThreadInv ti = quad_inv(m0, fdi, fdj);
         ThreadInv tu = quad_inv(m1, fdi, fdj);
         if (!two) tu.W = 0.f;
-        mbar_wait(&mbar[t % NB], (uint32_t)((t / NB) & 1));
-        if (two) mbar_wait(&mbar[te % NB], (uint32_t)((te / NB) & 1));
-        const uint32_t a0 = raw0 + (uint32_t)((t % NB) * p.raw_bytes) +
+        mbar_wait(&mbar[bt], pt0);
+        if (two) mbar_wait(&mbar[be], pe);
+        const uint32_t a0 = raw0 + (uint32_t)(bt * p.raw_bytes) +
                             (uint32_t)(((ti.nv - m0.v_org) * BW + (ti.nu - m0.u_org)) * 4) + nm;
-        const uint32_t a1 = raw0 + (uint32_t)((te % NB) * p.raw_bytes) +
+        const uint32_t a1 = raw0 + (uint32_t)(be * p.raw_bytes) +
                             (uint32_t)(((tu.nv - m1.v_org) * BW + (tu.nu - m1.u_org)) * 4) + nm;
+        bt = be + 1;  // the view after te
+        pt0 = pe;
+        if (bt == NB) {
+            bt = 0;
+            pt0 ^= 1u;
+        }
         if constexpr (RUN == 4)
             walk_views_quad2<BW>(tacc, a0, ti, a1, tu);
         else
