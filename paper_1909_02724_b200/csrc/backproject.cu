@@ -1719,8 +1719,20 @@ __device__ __forceinline__ ThreadInv quad_inv(const Meta& m, float fdi, float fd
     return t;
 }
 
+// IFDK_BOUNDS_CHECK builds (tools/gpu_bounds.sh; compute-sanitizer is not available on the
+// GPU pool): every tap the QUAD / QUINT walks read must lie in its staged box -- row below the
+// box height, the column and its right neighbour inside the row -- or the kernel traps.
+__device__ __forceinline__ void check_tap(uint32_t addr, uint32_t blo, int bw, int bh)
+{
+#ifdef IFDK_BOUNDS_CHECK
+    const int idx = (int)(addr - blo) >> 2;
+    if (addr < blo || idx / bw >= bh || idx % bw > bw - 2) __trap();
+#endif
+}
+
 template <int BW, int Q0, int NQ>
-__device__ __forceinline__ void quad_groups(f2x (&acc)[4 * NQ], uint32_t a0, const ThreadInv& t)
+__device__ __forceinline__ void quad_groups(f2x (&acc)[4 * NQ], uint32_t a0, const ThreadInv& t,
+                                            uint32_t blo = 0, int bh = 0)
 {
     constexpr uint32_t S = BW * 4;
     const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
@@ -1740,6 +1752,8 @@ __device__ __forceinline__ void quad_groups(f2x (&acc)[4 * NQ], uint32_t a0, con
         f2x h[5];  // rows n-1 .. n+3
 #pragma unroll
         for (int r = 0; r < 5; ++r) {
+            check_tap(adA + (r - 1) * S, blo, BW, bh);
+            check_tap(adB + (r - 1) * S, blo, BW, bh);
             const f2x a = pk2(lds32(adA + (r - 1) * S), lds32(adB + (r - 1) * S));
             const f2x b = pk2(lds32(adA + (r - 1) * S + 4), lds32(adB + (r - 1) * S + 4));
             h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
@@ -1760,25 +1774,27 @@ __device__ __forceinline__ void quad_groups(f2x (&acc)[4 * NQ], uint32_t a0, con
 // Two groups (16 TMEM columns: pair 4 q + m = slices 8 q + m / 8 q + 4 + m) of two views.
 template <int BW, int Q0>
 __device__ __forceinline__ void quad_sub2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
-                                          uint32_t a1, const ThreadInv& u)
+                                          uint32_t a1, const ThreadInv& u, uint32_t b0,
+                                          uint32_t b1, int bh)
 {
     f2x acc[8];
     tm_ld16(tacc + 8 * Q0, acc);
     tm_wait_ld();
-    quad_groups<BW, Q0, 2>(acc, a0, t);
-    quad_groups<BW, Q0, 2>(acc, a1, u);
+    quad_groups<BW, Q0, 2>(acc, a0, t, b0, bh);
+    quad_groups<BW, Q0, 2>(acc, a1, u, b1, bh);
     tm_st16(tacc + 8 * Q0, acc);
 }
 
 template <int BW>
 __device__ __forceinline__ void walk_views_quad2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
-                                                 uint32_t a1, const ThreadInv& u)
+                                                 uint32_t a1, const ThreadInv& u, uint32_t b0,
+                                                 uint32_t b1, int bh)
 {
     tm_wait_st();
-    quad_sub2<BW, 0>(tacc, a0, t, a1, u);
-    quad_sub2<BW, 2>(tacc, a0, t, a1, u);
-    quad_sub2<BW, 4>(tacc, a0, t, a1, u);
-    quad_sub2<BW, 6>(tacc, a0, t, a1, u);
+    quad_sub2<BW, 0>(tacc, a0, t, a1, u, b0, b1, bh);
+    quad_sub2<BW, 2>(tacc, a0, t, a1, u, b0, b1, bh);
+    quad_sub2<BW, 4>(tacc, a0, t, a1, u, b0, b1, bh);
+    quad_sub2<BW, 6>(tacc, a0, t, a1, u, b0, b1, bh);
 }
 
 // QUINT walk (walk 14, the default where dv/dk < 1/2, config 5): runs of five slices around a
@@ -1791,7 +1807,8 @@ __device__ __forceinline__ void walk_views_quad2(uint32_t tacc, uint32_t a0, con
 // 0, 1, 2) -- g_j in [-1, 1) exactly when 0.5 <= dv <= 1: six rows per five slices, 2.4 LDS.32
 // per update (QUAD 2.5) but a 2+2 tail per chunk.
 template <int BW, int Q0, int NQ, bool HI = false>
-__device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, const ThreadInv& t)
+__device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, const ThreadInv& t,
+                                             uint32_t blo = 0, int bh = 0)
 {
     constexpr uint32_t S = BW * 4;
     const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
@@ -1812,6 +1829,8 @@ __device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, co
         f2x h[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
+            check_tap(adA + (r - R0) * S, blo, BW, bh);
+            check_tap(adB + (r - R0) * S, blo, BW, bh);
             const f2x a = pk2(lds32(adA + (r - R0) * S), lds32(adB + (r - R0) * S));
             const f2x b = pk2(lds32(adA + (r - R0) * S + 4), lds32(adB + (r - R0) * S + 4));
             h[r] = fma2(du2, sub2(b, a), a);  // Alg. alg:subpixel lines 4-5
@@ -1842,7 +1861,8 @@ __device__ __forceinline__ void quint_groups(f2x (&acc)[5 * NQ], uint32_t a0, co
 
 // Slices 60, 61 (low half) and 62, 63 (high half) from rows n .. n+2 of their floors.
 template <int BW>
-__device__ __forceinline__ void quint_tail(f2x (&acc)[2], uint32_t a0, const ThreadInv& t)
+__device__ __forceinline__ void quint_tail(f2x (&acc)[2], uint32_t a0, const ThreadInv& t,
+                                           uint32_t blo = 0, int bh = 0)
 {
     constexpr uint32_t S = BW * 4;
     const f2x dv2 = pk2(t.dv, t.dv), dvm12 = pk2(t.dvm1, t.dvm1), W2 = pk2(t.W, t.W);
@@ -1856,6 +1876,8 @@ __device__ __forceinline__ void quint_tail(f2x (&acc)[2], uint32_t a0, const Thr
     f2x h[3];
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
+        check_tap(adA + r * S, blo, BW, bh);
+        check_tap(adB + r * S, blo, BW, bh);
         const f2x a = pk2(lds32(adA + r * S), lds32(adB + r * S));
         const f2x b = pk2(lds32(adA + r * S + 4), lds32(adB + r * S + 4));
         h[r] = fma2(du2, sub2(b, a), a);
@@ -1869,7 +1891,8 @@ __device__ __forceinline__ void quint_tail(f2x (&acc)[2], uint32_t a0, const Thr
 // Two QUINT groups (20 TMEM columns: pair 5 q + m = slices 10 q + m / 10 q + 5 + m) of two views.
 template <int BW, int Q0, bool HI>
 __device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
-                                           uint32_t a1, const ThreadInv& u)
+                                           uint32_t a1, const ThreadInv& u, uint32_t b0,
+                                           uint32_t b1, int bh)
 {
     f2x acc[10];
     {
@@ -1882,8 +1905,8 @@ __device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const Thr
         acc[8] = y[0];
         acc[9] = y[1];
     }
-    quint_groups<BW, Q0, 2, HI>(acc, a0, t);
-    quint_groups<BW, Q0, 2, HI>(acc, a1, u);
+    quint_groups<BW, Q0, 2, HI>(acc, a0, t, b0, bh);
+    quint_groups<BW, Q0, 2, HI>(acc, a1, u, b1, bh);
     {
         f2x x[8], y[2];
 #pragma unroll
@@ -1897,17 +1920,18 @@ __device__ __forceinline__ void quint_sub2(uint32_t tacc, uint32_t a0, const Thr
 
 template <int BW, bool HI>
 __device__ __forceinline__ void walk_views_quint2(uint32_t tacc, uint32_t a0, const ThreadInv& t,
-                                                  uint32_t a1, const ThreadInv& u)
+                                                  uint32_t a1, const ThreadInv& u, uint32_t b0,
+                                                  uint32_t b1, int bh)
 {
     tm_wait_st();
-    quint_sub2<BW, 0, HI>(tacc, a0, t, a1, u);
-    quint_sub2<BW, 2, HI>(tacc, a0, t, a1, u);
-    quint_sub2<BW, 4, HI>(tacc, a0, t, a1, u);
+    quint_sub2<BW, 0, HI>(tacc, a0, t, a1, u, b0, b1, bh);
+    quint_sub2<BW, 2, HI>(tacc, a0, t, a1, u, b0, b1, bh);
+    quint_sub2<BW, 4, HI>(tacc, a0, t, a1, u, b0, b1, bh);
     f2x acc[2];
     tm_ld4(tacc + 60, acc);
     tm_wait_ld();
-    quint_tail<BW>(acc, a0, t);
-    quint_tail<BW>(acc, a1, u);
+    quint_tail<BW>(acc, a0, t, b0, bh);
+    quint_tail<BW>(acc, a1, u, b1, bh);
     tm_st4(tacc + 60, acc);
 }
 
@@ -2036,6 +2060,7 @@ __global__ void __launch_bounds__(kThreads, 3)
         if (!two) tu.W = 0.f;
         mbar_wait(&mbar[bt], pt0);
         if (two) mbar_wait(&mbar[be], pe);
+        const int bt0 = bt;
         const uint32_t a0 = raw0 + (uint32_t)(bt * p.raw_bytes) +
                             (uint32_t)(((ti.nv - m0.v_org) * BW + (ti.nu - m0.u_org)) * 4) + nm;
         const uint32_t a1 = raw0 + (uint32_t)(be * p.raw_bytes) +
@@ -2046,10 +2071,11 @@ __global__ void __launch_bounds__(kThreads, 3)
             bt = 0;
             pt0 ^= 1u;
         }
+        const uint32_t b0 = raw0 + (uint32_t)(bt0 * p.raw_bytes), b1 = raw0 + (uint32_t)(be * p.raw_bytes);
         if constexpr (RUN == 4)
-            walk_views_quad2<BW>(tacc, a0, ti, a1, tu);
+            walk_views_quad2<BW>(tacc, a0, ti, a1, tu, b0, b1, p.box_h);
         else
-            walk_views_quint2<BW, RUN == 6>(tacc, a0, ti, a1, tu);
+            walk_views_quint2<BW, RUN == 6>(tacc, a0, ti, a1, tu, b0, b1, p.box_h);
         if ((te >= first_flush && ((te - first_flush) & (VB - 1)) == 0) || te == n - 1) {
             const int fi = tile_i * kTI + (warp & 1) * 8 + (lane & 7);
             const int fj = tile_j * kTJ + (warp >> 1) * 4 + (lane >> 3);
