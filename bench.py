@@ -272,7 +272,7 @@ def run_reference(args, spec, rank, world):
         "e2e": {"value": value, "unit": "GUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -861,10 +861,30 @@ def run_ours(args, spec, rank, world, local_rank):
         out["other_configs"] = others
     if iterative:
         out["iterative"] = iterative
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+_JSON_OUT = None
+
+
+def emit(out):
+    """The one JSON line, on the process's original stdout."""
+    f = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    f.write(json.dumps(out) + "\n")
+    f.flush()
+
+
+def route_stdout_to_stderr():
+    """Keep stdout for the JSON line alone: everything else written to fd 1 -- NCCL's version
+    banner at process-group init, library prints -- goes to stderr."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
 
 
 def main():
+    route_stdout_to_stderr()
     args = parse()
     import synth
 
