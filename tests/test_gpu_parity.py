@@ -492,7 +492,7 @@ def test_kslab_driver_single_rank_equals_reconstruct(torch_cuda):
             assert torch.equal(slab, ref[k0:k0 + nk]), (world, rank)
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(24))
 def test_bp_random_geometries(torch_cuda, seed):
     """Random scanners (magnification, pitches, non-square detectors and volumes, odd sizes,
     view offsets, detectors smaller or larger than the shadow) on a rough random Q: the patch
