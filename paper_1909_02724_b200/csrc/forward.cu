@@ -58,7 +58,43 @@ __device__ __forceinline__ void red_add_if(uint32_t addr, int v, uint32_t pred)
 
 struct __align__(16) Box {
     int u_org, v_org, w, h;
+    // the tile corner's invariants (fp64, split) and P_s in fp32: each thread adds its offset
+    // from the corner in fp32 (backproject.cu quad_inv, reading c-N2)
+    int uci, vci;
+    float ucf, vcf;
+    float uc, vc, zc, p0;
+    float p1, p3, p4, p5;
+    float p7, p8, pad0, pad1;
 };
+
+__device__ __forceinline__ float rcp_approx_fp(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
+// Per-(column, view) invariants from the corner values: u = u_c + (dx - u_c dz) / z (fp32
+// offsets dx, dz of the column from the corner, < 16 voxels), the same for v(kb).
+__device__ __forceinline__ ThreadInv corner_inv(const Box& m, float fdi, float fdj)
+{
+    ThreadInv t;
+    const float dx = fmaf(m.p0, fdi, m.p1 * fdj);
+    const float dy = fmaf(m.p3, fdi, m.p4 * fdj);
+    const float dz = fmaf(m.p7, fdi, m.p8 * fdj);
+    const float f = rcp_approx_fp(m.zc + dz);
+    const float su = fmaf(fmaf(-m.uc, dz, dx), f, m.ucf);
+    const float sv = fmaf(fmaf(-m.vc, dz, dy), f, m.vcf);
+    const float tu = __fadd_rd(su, 12582912.0f), tv = __fadd_rd(sv, 12582912.0f);
+    t.nu = m.uci + (int)(__float_as_uint(tu) - 0x4B400000u);
+    t.nv = m.vci + (int)(__float_as_uint(tv) - 0x4B400000u);
+    t.du = su - (tu - 12582912.0f);
+    t.fv0 = sv - (tv - 12582912.0f);
+    t.dv = m.p5 * f;
+    t.dvm1 = t.dv - 1.f;
+    t.W = f * f;
+    return t;
+}
 constexpr int kBoxRing = 16;
 
 template <bool SMALL_DV>
@@ -77,7 +113,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int i = tile_i * kTI + (lane & 7) * 2 + (warp & 1);
     const int j = tile_j * kTJ + (lane >> 3) * 4 + (warp >> 1);
     const bool active = i < p.Nx && j < p.Ny;
-    const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
+    const float fdi = (float)(min(i, p.Nx - 1) - tile_i * kTI);
+    const float fdj = (float)(min(j, p.Ny - 1) - tile_j * kTJ);
     const int kb = p.kb0 + (int)blockIdx.y * kKC;
     const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, kKC);
     const bool full = kv0 == 0 && kv1 == kKC;
@@ -109,16 +146,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     int ex;
     frexpf(xmax * p.qfactor, &ex);  // xmax qfactor < 2^ex
     const float scale = ldexpf(1.f, 30 - ex), inv_scale = ldexpf(1.f, ex - 30);
-    // patch box of view t: lanes 0-3 of warp 0 take the tile's corner columns at both chunk
-    // ends (u, v are linear-fractional in the column position: extremes sit at corners)
-    // Boxes are computed 8 views at a time, one view per warp (no warp waits at the per-view
-    // barrier for another's fp64 corner math).
-    auto make_box = [&](int t) {
-        if (t >= p.n_views) return;
+    // patch boxes of views t0 .. t0+7: lanes 4 v .. 4 v + 3 take view t0 + v at the tile's
+    // corner columns (u, v are linear-fractional in the column position: extremes sit at
+    // corners), so one warp computes eight views' boxes and corner invariants in one pass.
+    auto make_box8 = [&](int t0) {
+        const int t = t0 + (lane >> 2);
+        const bool valid = t < p.n_views;
         const int c = lane & 3;
         const double ci = (c & 1) ? min(tile_i * kTI + kTI, p.Nx) - 1 : tile_i * kTI;
         const double cj = (c & 2) ? min(tile_j * kTJ + kTJ, p.Ny) - 1 : tile_j * kTJ;
-        const ColInv ci0 = column_invariants(pt.P[t], ci, cj, (double)kb);
+        const double* Pc = pt.P[valid ? t : t0];
+        const ColInv ci0 = column_invariants(Pc, ci, cj, (double)kb);
         double umin = ci0.u, umax = ci0.u;
         double vmin = ci0.v + kv0 * ci0.dv, vmax = ci0.v + (kv1 - 1) * ci0.dv;
         if (vmin > vmax) { const double q = vmin; vmin = vmax; vmax = q; }
@@ -129,13 +167,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             vmin = fmin(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
             vmax = fmax(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
         }
-        if (lane == 0) {
+        if (valid && c == 0) {  // the base corner (tile_i * 16, tile_j * 16)
             Box b;
             b.u_org = (int)floor(umin) - 1;
             b.v_org = (int)floor(vmin) - 1;
             b.w = (int)floor(umax) - b.u_org + 3;
             b.h = (int)floor(vmax) - b.v_org + 3;
             if (b.w > p.box_w || b.h > p.box_h) __trap();  // the host bound is conservative
+            const double fu = floor(ci0.u), fv = floor(ci0.v);
+            b.uci = (int)fu;
+            b.vci = (int)fv;
+            b.ucf = (float)(ci0.u - fu);
+            b.vcf = (float)(ci0.v - fv);
+            b.uc = (float)ci0.u;
+            b.vc = (float)ci0.v;
+            b.zc = (float)ci0.z;
+            b.p0 = (float)Pc[0]; b.p1 = (float)Pc[1]; b.p3 = (float)Pc[3]; b.p4 = (float)Pc[4];
+            b.p5 = (float)Pc[5]; b.p7 = (float)Pc[7]; b.p8 = (float)Pc[8];
+            b.pad0 = b.pad1 = 0.f;
             box[t & (kBoxRing - 1)] = b;
         }
     };
@@ -166,14 +215,14 @@ __global__ void __launch_bounds__(kThreads, 2)
     };
 
     for (int e = tid; e < 2 * cap; e += kThreads) patch0[e] = 0;
-    make_box(warp);  // views 0 .. 7
+    if (warp == 0) make_box8(0);  // views 0 .. 7
     __syncthreads();
     // One barrier per view: splat view t into buffer t & 1 while view t-1's buffer is flushed
     // and the box of view t+1 is computed.
     for (int t = 0; t < p.n_views; ++t) {
         const Box b = box[t & (kBoxRing - 1)];
         int* const pa = patch0 + (t & 1) * cap;
-        const ThreadInv ti = split(column_invariants(pt.P[t], di, dj, (double)kb));
+        const ThreadInv ti = corner_inv(b, fdi, fdj);
         int* const base = pa + (ti.nv - b.v_org) * p.box_w + (ti.nu - b.u_org);
         const float ws1 = ti.du * scale, ws0 = (1.f - ti.du) * scale;  // columns nu, nu+1
         // Along k the column's contributions move down the detector rows (v affine in k, dv > 0):
@@ -268,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         if (t > 0) flush(t - 1);
         // views t+2 .. t+9 (slots of views t-1, t in use; t+1 already computed)
-        if (((t + 2) & 7) == 0) make_box(t + 2 + warp);
+        if (((t + 2) & 7) == 0 && warp == (((t + 2) >> 3) & 7)) make_box8(t + 2);
         __syncthreads();
     }
     if (p.n_views > 0) flush(p.n_views - 1);
