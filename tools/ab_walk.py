@@ -3,7 +3,8 @@
     python tools/ab_walk.py CONFIG WALK_A,WALK_B[,...] [n_views]
 
 Times one n_views launch (default 256) of each walk over the whole volume (config 5: k-slab 0
-of 8) with CUDA events and checks every volume is bitwise equal to the first walk's."""
+of 8) with CUDA events and checks every volume is bitwise equal to the first walk's.  A walk
+written W:R also sets the CTA raster band to R tile columns."""
 import sys
 
 import torch
@@ -24,7 +25,8 @@ def main(cfg, walks, n=256, reps=3):
     ifdk_filter(g, E, E)
     vols = {}
     for w in walks:
-        set_bp_variant(w)
+        wk, _, ra = str(w).partition(":")
+        set_bp_variant(int(wk), int(ra) if ra else 0)
         vol = torch.empty((nk, spec.Ny, spec.Nx), device="cuda")
         ifdk_backproject(g, E, 0, vol)
         torch.cuda.synchronize()
@@ -41,7 +43,7 @@ def main(cfg, walks, n=256, reps=3):
               flush=True)
         vols[w] = vol.cpu()
         del vol
-    set_bp_variant(0)
+    set_bp_variant(0, 0)
     for w in walks[1:]:
         eq = torch.equal(vols[walks[0]], vols[w])
         d = (vols[walks[0]] - vols[w]).abs().max().item()
@@ -51,4 +53,4 @@ def main(cfg, walks, n=256, reps=3):
 
 if __name__ == "__main__":
     a = sys.argv[1:]
-    main(int(a[0]), [int(w) for w in a[1].split(",")], int(a[2]) if len(a) > 2 else 256)
+    main(int(a[0]), a[1].split(","), int(a[2]) if len(a) > 2 else 256)
