@@ -102,8 +102,8 @@ __device__ __noinline__ void red_voxel(const BPParams& p, int k, int j, int i, f
 }
 
 // RED: the kernel instantiation may run the fused reduce (checked at run time, the reduce path
-// out of line).  The production walk (bp_tmem2_kernel) has a separate RED = false
-// instantiation without it: the mere call site cost it 1.2 % (2193 vs 2220 GUPS, config 4).
+// out of line).  The TMEM kernels (bp_quad2_kernel, bp_tmem2_kernel) have separate RED = false
+// instantiations without it: the mere call site cost 1.2 % (2193 vs 2220 GUPS, config 4).
 template <bool RED = true>
 __device__ __forceinline__ void put_voxel(const BPParams& p, float* q, int k, int j, int i,
                                           float v, bool overwrite)
