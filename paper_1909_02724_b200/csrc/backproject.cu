@@ -2154,8 +2154,9 @@ bool use_pair(const ifdk_geometry* g)
     return dv_max < 0.999;
 }
 
-// Tuning hook (ifdk_set_bp_variant): every walk it can select is bitwise equal to the
-// automatic choice, and the raster only reorders CTAs, so neither changes a result.
+// Tuning hook (ifdk_set_bp_variant): a walk of the automatic choice's family gives bitwise its
+// result (the QUAD / QUINT kernels are families of their own, equal to the others to fp32
+// rounding); the raster only reorders CTAs.
 std::atomic<int> g_walk_override{0}, g_raster_override{0};
 
 // Slices per floor of the k-walk.  Default where dv/dk < 1 for every z (all five configs):
