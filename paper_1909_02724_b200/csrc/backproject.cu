@@ -332,9 +332,10 @@ __device__ __forceinline__ void accumulate_view_smem(float (&acc)[KC], uint32_t 
                 asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
             }
             if (!FULL && (kk < kv0 || kk >= kv1)) continue;
-            float fr;
-            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
-            const uint32_t addr = clamp_floor<FULL>(bits * S + a0, lo_a, hi_a);
+            float fr;  // v = fv0 + kk dvf + kk dvi (whole rows): fp32 error ~ulp(KC), any dv
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dvf, fv0), &fr);
+            const uint32_t addr =
+                clamp_floor<FULL>((bits + (uint32_t)(kk * t.dvi)) * S + a0, lo_a, hi_a);
             const float2 p0 = lds64(addr);
             const float2 p1 = lds64(addr + S);
             const float h0 = fmaf(t.du, p0.y, p0.x);
@@ -509,8 +510,8 @@ __device__ __forceinline__ void accumulate_view_global(float (&acc)[KC], const f
             if ((kk & 3) == 0) asm volatile("mov.b32 %0, %0;" : "+f"(fv0));
             if (kk < kv0 || kk >= kv1) continue;
             float fr;
-            const uint32_t bits = floor_bits(fmaf((float)kk, t.dv, fv0), &fr);
-            const int row = t.nv + (int)(bits - 0x4B000000u);
+            const uint32_t bits = floor_bits(fmaf((float)kk, t.dvf, fv0), &fr);
+            const int row = t.nv + (int)(bits - 0x4B000000u) + kk * t.dvi;
             const float h0 = rowg(Qv, p, t, row), h1 = rowg(Qv, p, t, row + 1);
             acc[kk] = fmaf(t.W, fmaf(fr, h1 - h0, h0), acc[kk]);
         }
@@ -1716,6 +1717,8 @@ __device__ __forceinline__ ThreadInv quad_inv(const Meta& m, float fdi, float fd
     t.dv = m.p5 * f;
     t.dvm1 = t.dv - 1.f;
     t.W = f * f;
+    t.dvi = 0;  // the QUAD / QUINT walks need dv < 1
+    t.dvf = t.dv;
     return t;
 }
 

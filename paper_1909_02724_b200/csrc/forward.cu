@@ -93,6 +93,8 @@ __device__ __forceinline__ ThreadInv corner_inv(const Box& m, float fdi, float f
     t.dv = m.p5 * f;
     t.dvm1 = t.dv - 1.f;
     t.W = f * f;
+    t.dvi = 0;  // unused by the projector's walks
+    t.dvf = t.dv;
     return t;
 }
 constexpr int kBoxRing = 16;

@@ -58,6 +58,10 @@ __device__ __forceinline__ ColInv column_invariants(const double* P, double i, d
 struct ThreadInv {
     int nu, nv;
     float du, fv0, dv, dvm1, W;
+    // dv = dvi + dvf split in fp64 (the single-slice walk, any dv: v(kk) = fv0 + kk dvf in fp32
+    // plus kk dvi whole rows, so its fp32 part stays below KC + 1 instead of KC dv)
+    int dvi;
+    float dvf;
 };
 
 __device__ __forceinline__ ThreadInv split(const ColInv& c)
@@ -70,6 +74,9 @@ __device__ __forceinline__ ThreadInv split(const ColInv& c)
     t.fv0 = (float)(c.v - fv);
     t.dv = (float)c.dv;
     t.dvm1 = t.dv - 1.f;
+    const double fdv = floor(c.dv);
+    t.dvi = (int)fdv;
+    t.dvf = (float)(c.dv - fdv);
     t.W = (float)(c.f * c.f);  // W_dis = f^2, Alg. alg:bp line 8
     return t;
 }
