@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const bool active = i < p.Nx && j < p.Ny;
     const float fdi = (float)(min(i, p.Nx - 1) - tile_i * kTI);
     const float fdj = (float)(min(j, p.Ny - 1) - tile_j * kTJ);
+    const double di = (double)min(i, p.Nx - 1), dj = (double)min(j, p.Ny - 1);
     const int kb = p.kb0 + (int)blockIdx.y * kKC;
     const int kv0 = max(p.k0 - kb, 0), kv1 = min(p.k0 + p.nk - kb, kKC);
     const bool full = kv0 == 0 && kv1 == kKC;
@@ -224,7 +225,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int t = 0; t < p.n_views; ++t) {
         const Box b = box[t & (kBoxRing - 1)];
         int* const pa = patch0 + (t & 1) * cap;
-        const ThreadInv ti = corner_inv(b, fdi, fdj);
+        // dv < 1: fp32 offsets from the tile corner; many rows per slice: per-column fp64 with
+        // dv split into whole rows + an fp32 fraction (an fp32 dv would carry ~1e-7 dv per slice)
+        const ThreadInv ti = SMALL_DV ? corner_inv(b, fdi, fdj)
+                                      : split(column_invariants(pt.P[t], di, dj, (double)kb));
         int* const base = pa + (ti.nv - b.v_org) * p.box_w + (ti.nu - b.u_org);
         const float ws1 = ti.du * scale, ws0 = (1.f - ti.du) * scale;  // columns nu, nu+1
         // Along k the column's contributions move down the detector rows (v affine in k, dv > 0):
@@ -233,7 +237,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         // instead of four float atomics per slice.
         if (active) {
             float fr;
-            int cur = (int)(floor_bits(fmaf((float)kv0, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+            int cur = (int)(floor_bits(fmaf((float)kv0, ti.dvf, ti.fv0), &fr) - 0x4B000000u) +
+                      kv0 * ti.dvi;
             float A = 0.f, B = 0.f;
             auto add_row = [&](int r, float sv) {  // Alg. alg:subpixel lines 4-5, transposed
                 int* q = base + r * p.box_w;
@@ -297,7 +302,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int kk = 0; kk < kKC; ++kk) {
                     if (x[kk] == 0.f) continue;  // outside the slab (and empty voxels)
                     const int n =
-                        (int)(floor_bits(fmaf((float)kk, ti.dv, ti.fv0), &fr) - 0x4B000000u);
+                        (int)(floor_bits(fmaf((float)kk, ti.dvf, ti.fv0), &fr) - 0x4B000000u) +
+                        kk * ti.dvi;  // whole rows of dv added as integers (backproject.cu walk 1)
                     if (n != cur) {  // the walk left row cur (n > cur)
                         if (A != 0.f) add_row(cur, A);
                         if (n == cur + 1) {

@@ -200,3 +200,13 @@ def test_mlem_matches_oracle(torch_cuda, block, n_iter):
     x = mlem(Geometry.from_spec(spec), torch.from_numpy(b32).cuda(), n_iter, block=block)
     ref = oracle.mlem(og, b32.astype(np.float64), n_iter, block=block)
     assert_parity(x.cpu().numpy(), ref, VOL_RMSE, VOL_MAX_REL, f"mlem block={block}")
+
+
+def test_fp_many_detector_rows_per_slice(torch_cuda):
+    """The projector's large-dv walk (1.9-3.3 detector rows per slice; larger patches exceed its
+    shared memory and are refused): per-column fp64 invariants with dv split into whole rows +
+    an fp32 fraction, as the back-projector's single-slice walk."""
+    spec = _spec(35, 21, 49, 14, 33, 62, d=1035.113914283941, D=1384.110376984815,
+                 det_mm=180.43609777816965, cube_mm=409.8307371445136)
+    got, ref = _fp_case(torch_cuda, spec, 0, 35, 0, 62)
+    assert_parity(got, ref, VOL_RMSE, VOL_MAX_REL, "fp 1.9-3.3 detector rows per slice")
